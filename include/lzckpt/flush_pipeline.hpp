@@ -1,0 +1,134 @@
+// Host-to-storage writer for one rank (streaming flush, header last).
+//
+// Public contract is the reference's (proj/core/include/lzckpt/flush_pipeline.hpp:38-120,
+// src/flush_pipeline.cpp:50-263): files registered with fixed header offsets,
+// payload chunks announced in byte order per segment, per-entry FNV-1a folded
+// as bytes stream through, header written last (a file without a valid header
+// is incomplete), optional fsync, segment released FIFO, abandon and injected
+// mid-flush failure.
+//
+// Unlike the reference (one worker holding the pipeline mutex across pwrite
+// and hashing, flush_pipeline.cpp:139-241, which serializes the copy channel
+// behind the disk), enqueue_flush only records the chunk; a pool of worker
+// threads pwrites pieces in parallel and hashes different entries in
+// parallel, each entry's FNV still folded strictly in byte order.
+#pragma once
+
+#include <chrono>
+#include <condition_variable>
+#include <cstdint>
+#include <deque>
+#include <filesystem>
+#include <functional>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "lzckpt/buffer_pool.hpp"
+#include "lzckpt/checksum.hpp"
+#include "lzckpt/format.hpp"
+
+namespace lzckpt {
+
+struct FlushConfig {
+  double storage_bandwidth_Bps = 0;  // <= 0: unthrottled
+  bool fsync_on_finalize = true;
+  // B200-host extensions
+  unsigned threads = 0;              // worker pool size; 0 = auto (<= 8)
+  uint64_t write_piece = 8ull << 20; // max bytes per pwrite job
+};
+
+enum class FlushFileState { Pending, Persisted, Abandoned };
+
+class FlushPipeline {
+ public:
+  using FileDoneCallback = std::function<void(uint64_t file_id, FlushFileState)>;
+
+  FlushPipeline(HostBufferPool& pool, FlushConfig config);
+  ~FlushPipeline();
+  FlushPipeline(const FlushPipeline&) = delete;
+  FlushPipeline& operator=(const FlushPipeline&) = delete;
+
+  uint64_t register_file(std::filesystem::path path, CheckpointFileHeader header,
+                         uint64_t segment_id, FileDoneCallback on_done = {});
+  void enqueue_flush(uint64_t segment_id, uint64_t segment_offset, uint64_t length);
+  void abandon(uint64_t file_id);
+  void inject_failure_after(uint64_t bytes);
+  void drain();
+  FlushFileState file_state(uint64_t file_id) const;
+
+  uint64_t bytes_written() const;
+  uint64_t files_persisted() const;
+  size_t queue_depth() const;
+
+ private:
+  struct EntryCursor {
+    uint64_t begin = 0;     // payload-relative
+    uint64_t end = 0;
+    uint64_t resident = 0;  // bytes [begin, resident) are in the pool
+    uint64_t hashed = 0;
+    uint64_t state = Fnv64::kOffset;  // FNV-1a over [begin, hashed)
+    bool busy = false;
+  };
+  struct FileRecord {
+    std::filesystem::path path;
+    CheckpointFileHeader header;
+    uint64_t segment_id = 0;
+    uint64_t header_size = 0;
+    uint64_t expected = 0;
+    uint64_t enqueued = 0;   // next in-order chunk offset
+    uint64_t accounted = 0;  // written + starved bytes
+    uint32_t jobs = 0;       // outstanding jobs touching this file
+    const std::byte* base = nullptr;
+    std::vector<EntryCursor> entries;
+    size_t entries_done = 0;
+    int fd = -1;
+    bool abandoned = false;
+    bool finalizing = false;
+    bool finalized = false;
+    FlushFileState state = FlushFileState::Pending;
+    FileDoneCallback on_done;
+  };
+  struct Job {
+    bool hash = false;
+    uint64_t file = 0;
+    uint64_t offset = 0;  // write: payload offset
+    uint64_t length = 0;  // write: bytes
+    size_t entry = 0;     // hash: entry index
+  };
+
+  void worker_loop();
+  void run_write(FileRecord& f, const Job& j);
+  void run_hash(uint64_t file_id, size_t entry);
+  void maybe_finalize(std::unique_lock<std::mutex>& lk, uint64_t file_id);
+  void release_in_order(std::unique_lock<std::mutex>& lk);
+  void fail_locked(const std::string& why);
+
+  HostBufferPool& pool_;
+  const FlushConfig config_;
+
+  mutable std::mutex mu_;
+  std::condition_variable work_cv_;
+  std::condition_variable done_cv_;
+  std::deque<Job> jobs_;
+  std::unordered_map<uint64_t, uint64_t> seg_to_file_;
+  std::unordered_map<uint64_t, FileRecord> files_;
+  std::deque<uint64_t> release_order_;  // registration order
+  uint64_t next_file_ = 1;
+  uint64_t pending_files_ = 0;
+  uint32_t callbacks_in_flight_ = 0;
+  uint32_t busy_workers_ = 0;
+  uint64_t bytes_written_ = 0;
+  uint64_t files_persisted_ = 0;
+  int64_t fail_after_ = -1;
+  std::string error_;
+  bool stopping_ = false;
+
+  std::mutex pace_mu_;
+  std::chrono::steady_clock::time_point pace_point_{};
+  std::vector<std::thread> workers_;
+};
+
+}  // namespace lzckpt
