@@ -1,0 +1,494 @@
+"""Benchmark of the B200 lazy D2H snapshot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One "step" = one checkpoint of the rank's shard through the public engine
+API: capture() (flatten, batched small-leaf snapshot, pinned-ring
+reservation, device issue of every copy) until the lazy fence is ready (all
+payload bytes resident in pinned host memory). Workload at N=1 is
+BASELINE.json configs[1]: a LLaMA-2-7B-shaped shard (fp32 params + fp32
+master + Adam m/v, 4+12 B/param, 1164 tensors, 107.8 GB) generated in HBM.
+N>1 runs one process per GPU (torchrun), each snapshotting its own C2-sized
+shard of a dp=N plan (weak scaling, no collective on the data path).
+
+The JSON line carries: value (aggregate snapshot GB/s, device-event timed,
+max over ranks), the copy-variant sweep (gather kernel / copy engine /
+per-size hybrid), roofline vs the PCIe Gen5 x16 host link, the per-iteration
+stall under a synthetic bf16 fwd/bwd load with the device-side fence,
+e2e (capture -> files durable on disk through the public API), the CPU
+reference engine timed on this box's cores, clocks during the timed region,
+and the number of our kernel launches.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "D2H snapshot GB/s (per GPU, 8-GPU aggregate); per-iteration ckpt stall ms"
+PCIE_GEN5_X16_GBPS = 64.0  # BASELINE.json north_star host-link roofline (nominal, per direction)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md recipe)
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline: the unmodified reference engine (oracle/_ref)
+
+
+def run_reference(steps: int, warmup: int, fsync: bool = True):
+    """Reference CPU engine (oracle/_ref/ref_snapshot, built from the
+    reference's own sources) on a bounded sample of the C2 workload: one
+    LLaMA-7B decoder layer's params + fp32 master + Adam m/v (3.24 GB, same
+    tensor shapes and 4+12 B/param). Metric = payload / (capture + lazy
+    barrier), the reference's stall."""
+    from paper_2406_10707_b200.workloads import llama_layer_sample
+    drv = os.path.join(ROOT, "oracle", "_ref", "ref_snapshot")
+    if not os.path.exists(drv):
+        return None
+    w = llama_layer_sample()
+    tmp = tempfile.mkdtemp(prefix="lzk_refarm_", dir=ROOT)
+    try:
+        spec = w.write_spec(os.path.join(tmp, "sample.spec"))
+        r = subprocess.run([drv, "--spec", spec, "--root", os.path.join(tmp, "ckpt"), "--repeat",
+                            str(steps + warmup), "--digest", "0", "--fsync", "1" if fsync else "0",
+                            "--keep-last", "1"], capture_output=True, text=True, timeout=1800)
+        res = json.loads(r.stdout)
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+    st = res["ranks"][0]["steps"][warmup:]
+    payload = st[0]["payload"]
+    stall = [s["capture_s"] + s["barrier_s"] for s in st]
+    persisted = [s["persisted_s"] for s in st]
+    return {"payload": payload, "steps": len(st), "stall_s": stall, "persisted_s": persisted,
+            "snapshot_gbps": payload * len(st) / sum(stall) / 1e9,
+            "persisted_gbps": payload * len(st) / sum(persisted) / 1e9,
+            "sample": f"{w.name}: 1 LLaMA-7B decoder layer, {len(w.leaves)} tensors, {payload} B payload per step, "
+                      f"fsync={int(fsync)}"}
+
+
+def cpu_info():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    res = run_reference(args.steps, args.warmup)
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_snapshot not built"}))
+        return
+    v = res["snapshot_gbps"]
+    line = {"metric": METRIC, "value": round(v, 4), "unit": "GB/s", "impl": "reference", "n_gpus": world,
+            "steps": res["steps"], "warmup": args.warmup,
+            "ms_per_step": round(1e3 * statistics.mean(res["stall_s"]), 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": "c2-llama7b (bounded sample: 1 decoder layer)", "engine": "reference lzckpt CPU",
+                       "host": cpu_info()},
+            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 2, "kind": "reference",
+                             "sample": res["sample"]},
+            "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "persisted_gbps": round(res["persisted_gbps"], 4)}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def fits_host(bytes_per_rank: int, world: int) -> bool:
+    try:
+        avail = next(int(l.split()[1]) * 1024 for l in open("/proc/meminfo") if l.startswith("MemAvailable"))
+    except (OSError, StopIteration):
+        return True
+    return bytes_per_rank * world <= 0.75 * avail
+
+
+def main_ours(args, rank, world, local_rank):
+    import numpy as np  # noqa: F401
+    import torch
+    import torch.distributed as dist
+
+    import paper_2406_10707_b200 as lz
+    from paper_2406_10707_b200.workloads import llama7b_shard
+
+    torch.cuda.set_device(local_rank)
+    dev = local_rank
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # CPU reference baseline first (rank 0, N=1 only), before we pin memory
+    cpu_base = None
+    if rank == 0 and world == 1 and not args.skip_cpu_baseline:
+        t0 = time.time()
+        cpu_base = run_reference(steps=2, warmup=1)
+        log(f"[bench] reference CPU baseline: {cpu_base and round(cpu_base['snapshot_gbps'], 3)} GB/s "
+            f"({time.time() - t0:.1f} s)")
+
+    layers = args.layers
+    w = llama7b_shard(layers=layers, dp=world, rank=rank)
+    while not fits_host(int(w.total_bytes * 1.03), world) and layers > 1:
+        layers -= 1
+        w = llama7b_shard(layers=layers, dp=world, rank=rank)
+    tmp = tempfile.mkdtemp(prefix=f"lzk_bench_r{rank}_", dir=ROOT)
+    try:
+        spec = w.write_spec(os.path.join(tmp, "w.spec"))
+        t0 = time.time()
+        built = lz.build_workload(spec, dev)
+        torch.cuda.synchronize()
+        log(f"[bench] rank {rank}: workload {w.name} layers={layers} {built.bytes / 1e9:.2f} GB "
+            f"{len(w.leaves)} tensors built in {time.time() - t0:.1f} s")
+
+        # host-link copy-engine peak on this box (one 4 GiB pinned DMA)
+        src = torch.empty(4 << 30, dtype=torch.uint8, device="cuda")
+        dst = torch.empty(4 << 30, dtype=torch.uint8, pin_memory=True)
+        ce_best = 0.0
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dst.copy_(src, non_blocking=True)
+            e1.record()
+            e1.synchronize()
+            ce_best = max(ce_best, (4 << 30) / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+        del src, dst
+        torch.cuda.empty_cache()
+
+        pool_bytes = int(built.bytes * 1.01) + (256 << 20)
+        cfg = lz.EngineConfig(checkpoint_root=os.path.join(tmp, "ckpt"), host_buffer_bytes=pool_bytes,
+                              large_leaf_threshold=1 << 20, fsync_on_finalize=False, flush_discard=True,
+                              hugepages=True, device=dev)
+        t0 = time.time()
+        eng = lz.Engine(cfg, built.topo, built.rank)
+        log(f"[bench] rank {rank}: pinned {pool_bytes / 1e9:.1f} GB pool in {time.time() - t0:.1f} s")
+        snap_stream = torch.cuda.ExternalStream(eng.snapshot_stream, device=dev)
+        plan = lz.plan_checkpoint(built.topo, built.model, built.step)
+
+        def one_step(step):
+            """capture -> fence-ready; returns (device ms, host ms, payload, capture ms)."""
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            h0 = time.perf_counter()
+            e0.record(snap_stream)
+            t = eng.capture(plan, built.tree, step)
+            e1.record(snap_stream)
+            h1 = time.perf_counter()
+            eng.update_barrier(t)
+            h2 = time.perf_counter()
+            eng.wait_persisted(t)  # discard tier: releases the pinned segment
+            return e0.elapsed_time(e1), (h2 - h0) * 1e3, t.payload_bytes(), (h1 - h0) * 1e3
+
+        # ---- copy-variant sweep (same bytes, each variant) ----
+        variants = {}
+        for name, kw in (("gather_kernel", dict(force_kernel=True)),
+                         ("copy_engine", dict(force_copy_engine=True)),
+                         ("hybrid", dict(ce_threshold=2 << 20))):
+            eng.set_copy_variant(**kw)
+            barrier()
+            one_step(1)
+            ms = []
+            for s in range(2):
+                barrier()
+                dms, hms, payload, _ = one_step(2 + s)
+                ms.append(max(dms, hms))
+            variants[name] = round(payload / (statistics.mean(ms) * 1e-3) / 1e9, 3)
+            log(f"[bench] rank {rank}: variant {name}: {variants[name]} GB/s")
+        best = max(("gather_kernel", "copy_engine", "hybrid"), key=lambda k: variants[k])
+        eng.set_copy_variant(**{"gather_kernel": dict(force_kernel=True),
+                                "copy_engine": dict(force_copy_engine=True),
+                                "hybrid": dict(ce_threshold=2 << 20)}[best])
+
+        # ---- timed region ----
+        for s in range(args.warmup):
+            barrier()
+            one_step(10 + s)
+        launches0 = lz.kernel_launches()
+        stats0 = eng.snapshot_stats()
+        dev_ms, host_ms, cap_ms = [], [], []
+        barrier()
+        with ClockSampler(dev) as clocks:
+            for s in range(args.steps):
+                barrier()
+                dms, hms, payload, cms = one_step(100 + s)
+                dev_ms.append(dms)
+                host_ms.append(hms)
+                cap_ms.append(cms)
+            barrier()
+        launches = lz.kernel_launches() - launches0
+        stats1 = eng.snapshot_stats()
+        step_ms = [max(a, b) for a, b in zip(dev_ms, host_ms)]
+        t_total = max_over_ranks(sum(step_ms) * 1e-3)
+        agg_bytes = sum_over_ranks(float(payload * args.steps))
+        value = agg_bytes / t_total / 1e9
+        per_gpu = payload * args.steps / (sum(step_ms) * 1e-3) / 1e9
+        clk = clocks.summary()
+
+        # ---- per-iteration stall under synthetic fwd/bwd (device-side fence) ----
+        stall = None
+        if not args.skip_train:
+            stall = train_loop(lz, torch, eng, plan, built, payload, per_gpu, barrier)
+
+        # ---- e2e: public API, files durable on local disk ----
+        e2e = None
+        if not args.skip_e2e:
+            eng.close()
+            del eng
+            e2e = e2e_persisted(lz, torch, dev, tmp, args)
+
+        if rank == 0:
+            kernel_gbps = variants["gather_kernel"]
+            line = {
+                "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(statistics.mean(step_ms), 3),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+                "data": "synthetic (splitmix64 generated in HBM)",
+                "config": {"workload": f"c2-llama7b shard per GPU (configs[1]; {layers} layers, 4+12 B/param)",
+                           "payload_bytes_per_gpu": payload, "tensors": len(w.leaves),
+                           "variant": best, "large_leaf_threshold": 1 << 20, "chunk_quantum": 64 << 20,
+                           "flush_tier": "host-memory (discard) for the timed steps; storage flush in e2e",
+                           "l2": "inputs (>100 GB) exceed L2 (126 MB)", "parallelism": f"dp{world} weak"},
+                "per_gpu_gbps": round(per_gpu, 3),
+                "capture_host_ms": round(statistics.mean(cap_ms), 3),
+                "variants_gbps": variants,
+                "roofline": {"bound": "pcie-host-link", "achieved": round(per_gpu, 3), "peak": PCIE_GEN5_X16_GBPS,
+                             "unit": "GB/s", "frac": round(per_gpu / PCIE_GEN5_X16_GBPS, 4), "traffic": None,
+                             "peak_measured_ce": round(ce_best, 3),
+                             "frac_of_measured_ce": round(per_gpu / ce_best, 4),
+                             "kernel": {"name": "lzk_gather_kernel", "achieved": kernel_gbps,
+                                        "frac": round(kernel_gbps / PCIE_GEN5_X16_GBPS, 4)},
+                             "algorithmic_bytes_per_step": payload},
+                "stall": stall,
+                "e2e": e2e,
+                "cpu_baseline": None if cpu_base is None else {
+                    "value": round(cpu_base["snapshot_gbps"], 4), "unit": "GB/s", "cores": 2, "kind": "reference",
+                    "sample": cpu_base["sample"], "persisted_gbps": round(cpu_base["persisted_gbps"], 4),
+                    "host": cpu_info()},
+                "clocks": clk,
+                "gpu_launches": int(launches),
+                "copy_engine_dmas": int(stats1["ce_copies"] - stats0["ce_copies"]),
+            }
+            print(json.dumps(line), flush=True)
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+
+
+def train_loop(lz, torch, eng, plan, built, payload, gbps, barrier):
+    """Checkpoint every iteration under a synthetic bf16 fwd/bwd sized so that
+    t_fb >= payload / snapshot rate. Iteration = capture ->
+    fwd/bwd GEMMs -> lazy fence (device-side, update_barrier_on_stream) ->
+    optimizer step on a registered tensor. Stall = iteration time with
+    checkpointing minus without."""
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.bfloat16, device="cuda")
+    b = torch.randn(n, n, dtype=torch.bfloat16, device="cuda")
+    c = torch.empty(n, n, dtype=torch.bfloat16, device="cuda")
+    comp = torch.cuda.Stream()
+    with torch.cuda.stream(comp):
+        for _ in range(10):
+            torch.matmul(a, b, out=c)
+    comp.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(comp)
+    with torch.cuda.stream(comp):
+        for _ in range(50):
+            torch.matmul(a, b, out=c)
+    e1.record(comp)
+    e1.synchronize()
+    per_mm = e0.elapsed_time(e1) / 50
+    t_snap_ms = payload / (gbps * 1e9) * 1e3
+    n_mm = max(1, int(1.1 * t_snap_ms / per_mm))
+    opt = torch.zeros(64 << 20, dtype=torch.float32, device="cuda")  # the "optimizer state" we mutate
+    opt_region = lz.DeviceRegion.wrap(opt)
+
+    def iteration(step, ckpt: bool, device_fence: bool):
+        h0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(comp)
+        t = eng.capture(plan, built.tree, step) if ckpt else None
+        h1 = time.perf_counter()
+        with torch.cuda.stream(comp):
+            for _ in range(n_mm):
+                torch.matmul(a, b, out=c)  # forward + backward stand-in
+        if ckpt:
+            if device_fence:
+                eng.update_barrier_on_stream(t, comp.cuda_stream)
+            else:
+                comp.synchronize()
+                eng.update_barrier(t)
+        h2 = time.perf_counter()
+        with torch.cuda.stream(comp):
+            opt.add_(1.0)  # optimizer step: mutates state after the fence
+        opt_region.bump_version()
+        e1.record(comp)
+        e1.synchronize()
+        h3 = time.perf_counter()
+        if ckpt:
+            eng.wait_persisted(t)
+        return e0.elapsed_time(e1), (h1 - h0) * 1e3, (h2 - h1) * 1e3, (h3 - h0) * 1e3
+
+    barrier()
+    for s in range(2):
+        iteration(500 + s, False, True)
+    base = [iteration(510 + s, False, True)[3] for s in range(3)]
+    iteration(520, True, True)
+    dev_fence = [iteration(530 + s, True, True) for s in range(3)]
+    iteration(540, True, False)
+    host_fence = [iteration(550 + s, True, False) for s in range(2)]
+    base_ms = statistics.mean(base)
+    it_ms = statistics.mean(x[3] for x in dev_fence)
+    it_host_ms = statistics.mean(x[3] for x in host_fence)
+    return {"t_fwd_bwd_ms": round(n_mm * per_mm, 2), "iter_no_ckpt_ms": round(base_ms, 2),
+            "iter_ckpt_ms": round(it_ms, 2), "stall_ms": round(it_ms - base_ms, 2),
+            "capture_host_ms": round(statistics.mean(x[1] for x in dev_fence), 3),
+            "iter_overhead": round((it_ms - base_ms) / base_ms, 4),
+            "host_fence": {"iter_ckpt_ms": round(it_host_ms, 2), "stall_ms": round(it_host_ms - base_ms, 2),
+                           "iter_overhead": round((it_host_ms - base_ms) / base_ms, 4)},
+            "fence": "update_barrier_on_stream (device-side)", "gemm": "bf16 8192^3 torch.matmul x%d" % n_mm}
+
+
+def e2e_persisted(lz, torch, dev, tmp, args):
+    """Public API end to end with durable files: capture -> update_barrier ->
+    wait_persisted (pwrite + per-entry FNV + header last + fsync) on a
+    bounded C2 slice that fits local disk (1 decoder layer + embeddings)."""
+    from paper_2406_10707_b200.workloads import llama7b_shard
+    w = llama7b_shard(layers=2, vocab=8000, name="c2-slice-2l")
+    spec = w.write_spec(os.path.join(tmp, "e2e.spec"))
+    built = lz.build_workload(spec, dev)
+    root = os.path.join(tmp, "e2e_ckpt")
+    cfg = lz.EngineConfig(checkpoint_root=root, host_buffer_bytes=int(built.bytes * 1.01) + (64 << 20),
+                          fsync_on_finalize=True, device=dev)
+    eng = lz.Engine(cfg, built.topo, built.rank)
+    plan = lz.plan_checkpoint(built.topo, built.model, built.step)
+    times = []
+    for s in range(1 + 2):
+        torch.cuda.synchronize()
+        h0 = time.perf_counter()
+        t = eng.capture(plan, built.tree, 700 + s)
+        eng.update_barrier(t)
+        eng.wait_persisted(t)
+        dt = time.perf_counter() - h0
+        if s >= 1:
+            times.append(dt)
+        payload = t.payload_bytes()
+        shutil.rmtree(os.path.join(root, f"step-{700 + s}"), ignore_errors=True)
+    eng.close()
+    v = payload * len(times) / sum(times) / 1e9
+    return {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": payload,
+            "workload": f"{w.name} ({payload} B payload, {len(w.leaves)} tensors)",
+            "path": "capture -> update_barrier -> wait_persisted, fsync, local disk", "steps": len(times)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--layers", type=int, default=32, help="LLaMA-7B layers per shard (32 = full C2)")
+    ap.add_argument("--skip-train", action="store_true")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("[bench] warmup raised to 3 (timing rules)")
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        main_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -38,9 +38,13 @@ struct FlushConfig {
   // B200-host extensions
   unsigned threads = 0;              // worker pool size; 0 = auto (<= 8)
   uint64_t write_piece = 8ull << 20; // max bytes per pwrite job
+  // Host-memory tier only: no file is created, nothing is hashed or written;
+  // a segment is released as soon as all of its bytes are resident. For
+  // measuring the D2H snapshot stage on shards larger than local storage.
+  bool discard = false;
 };
 
-enum class FlushFileState { Pending, Persisted, Abandoned };
+enum class FlushFileState { Pending, Persisted, Abandoned, Discarded };
 
 class FlushPipeline {
  public:

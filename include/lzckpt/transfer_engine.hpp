@@ -7,11 +7,12 @@
 //
 // Underneath it is B200-native:
 //  * DeviceRegion owns (or wraps) real HBM;
-//  * unpaced submissions are launched on a low-priority snapshot stream at
-//    submit time: tensors below SnapshotOptions::ce_threshold go through ONE
-//    multi-tensor gather kernel launch per group (lzk_gather_d2h), larger
+//  * unpaced submissions are cut into groups on the caller (host metadata
+//    only) and issued by a per-engine issuer thread onto a low-priority
+//    snapshot stream: tensors below SnapshotOptions::ce_threshold go through
+//    ONE multi-tensor gather kernel launch per group (lzk_gather_d2h), larger
 //    ones through the copy engines (lzk_ce_copy_d2h); a CUDA event closes
-//    every group;
+//    every group. capture() therefore never blocks on the device queue;
 //  * one completion thread per rank waits on group events in FIFO order and
 //    only then decides torn-ness, marks segments Filled and announces chunks,
 //    so announcement order and the verdict-before-final-chunk rule are the
@@ -34,9 +35,9 @@
 #include <vector>
 
 #include "lzckpt/buffer_pool.hpp"
+#include "lzk_cuda.h"
 
-struct lzk_stream;
-struct lzk_event;
+
 
 namespace lzckpt {
 
@@ -160,6 +161,9 @@ class TransferEngine {
   bool fence_on_stream(uint64_t ticket, void* cuda_stream);
   bool ticket_complete(uint64_t ticket) const;
   const SnapshotOptions& options() const { return opts_; }
+  // Changes the variant selection for subsequent submissions (device and
+  // stream priority are fixed at construction).
+  void set_options(const SnapshotOptions& o);
   int device() const { return device_; }
   lzk_stream* stream() const { return stream_; }
 
@@ -181,25 +185,31 @@ class TransferEngine {
     bool last = false;
   };
   struct Group {
+    uint64_t ticket = 0;
+    bool paced = false;          // copied chunk by chunk by the completion thread
     std::vector<Piece> pieces;
-    lzk_event* done = nullptr;  // null: paced group (copied by the worker)
-    uint64_t tasks_finished = 0;
+    std::vector<lzk_copy_desc> kernel;  // gather-kernel descriptors (small tensors)
+    std::vector<lzk_copy_desc> dma;     // copy-engine descriptors (large tensors)
+    uint32_t kernel_ctas = 0;    // gather grid for this group
+    lzk_event* done = nullptr;   // recorded after the group's device work
+    bool issue_failed = false;
   };
   struct TicketProgress {
     uint64_t expected = 0;
     uint64_t completed = 0;
+    uint64_t unissued = 0;       // groups queued but not yet on the device
     bool torn = false;
     bool device_issued = true;
     lzk_event* last_event = nullptr;
     std::vector<std::shared_ptr<CopyTask>> tasks;  // for fence versions
   };
 
+  void issuer_loop();
   void worker_loop();
   void run_device_group(Group& g);
   void run_paced_group(Group& g);
-  void finish_piece(const Piece& p, std::vector<std::shared_ptr<CopyTask>>& torn_out);
-  void issue_groups(uint64_t ticket, const std::vector<std::shared_ptr<CopyTask>>& tasks,
-                    std::deque<Group>& out);
+  void build_groups(const std::vector<std::shared_ptr<CopyTask>>& tasks, std::deque<Group>& out);
+  void issue(Group& g);
   lzk_event* take_event();
   void give_event(lzk_event* e);
 
@@ -211,20 +221,26 @@ class TransferEngine {
   ChunkCallback chunk_cb_;
   TornCallback torn_cb_;
 
-  std::mutex submit_mu_;  // keeps device launch order == queue order
+  std::mutex opts_mu_;
   mutable std::mutex mu_;
+  std::condition_variable issue_cv_;
+  std::condition_variable issued_cv_;
   std::condition_variable work_cv_;
   std::condition_variable progress_cv_;
-  std::deque<Group> queue_;
+  std::deque<Group> issue_queue_;  // built on the caller, issued by issuer_
+  std::deque<Group> queue_;        // issued, awaiting completion on worker_
   std::unordered_map<uint64_t, TicketProgress> tickets_;
   std::vector<lzk_event*> free_events_;
   uint64_t in_flight_ = 0;
+  bool issuing_ = false;
   bool stopping_ = false;
+  bool issuer_done_ = false;
   Stats stats_;
 
   std::atomic<uint64_t> bytes_submitted_{0};
   std::atomic<uint64_t> bytes_delivered_{0};
   std::chrono::steady_clock::time_point pace_point_{};
+  std::thread issuer_;
   std::thread worker_;
 };
 

@@ -193,6 +193,7 @@ typedef struct lzckpt_engine_config {
   int force_kernel;
   int force_copy_engine;
   int hugepages;
+  int flush_discard;          /* host-memory tier only (no files) */
 } lzckpt_engine_config;
 void lzckpt_engine_config_defaults(lzckpt_engine_config* c);
 
@@ -232,6 +233,9 @@ typedef struct lzckpt_snapshot_stats {
 int lzckpt_engine_snapshot_stats(const lzckpt_engine* e, lzckpt_snapshot_stats* out);
 /* bytes the flush pipeline has written, files it persisted */
 int lzckpt_engine_flush_stats(const lzckpt_engine* e, uint64_t* bytes_written, uint64_t* files_persisted);
+/* Switches the D2H variant for later captures (B200 tuning knob). */
+int lzckpt_engine_set_copy_variant(lzckpt_engine* e, uint64_t ce_threshold, int force_kernel, int force_copy_engine,
+                                   uint32_t kernel_ctas, uint64_t group_bytes);
 /* the engine's snapshot stream (cudaStream_t) */
 void* lzckpt_engine_snapshot_stream(const lzckpt_engine* e);
 

@@ -48,6 +48,7 @@ struct Opts {
   bool digest = true;
   bool restore = false;
   std::string mode = "engine";
+  bool keep_last = false;  // delete each step's directory once the next persisted
 };
 
 double secs(clk::time_point a, clk::time_point b) {
@@ -163,6 +164,10 @@ std::string run_rank(const Opts& o, const wspec::Spec& s, const std::string& spe
                   (unsigned long long)ticket->payload_bytes(), secs(t0, t1), secs(t1, t2),
                   secs(t0, t3));
     out += head;
+    if (o.keep_last && last) {
+      std::error_code ec;
+      fs::remove_all(o.root / step_dirname(last->step()) / rank_dirname(rank), ec);
+    }
     last = ticket;
   }
   out += "],\"files\":[";
@@ -230,6 +235,7 @@ int main(int argc, char** argv) {
     else if (a == "--digest") o.digest = next() == "1";
     else if (a == "--restore") o.restore = next() == "1";
     else if (a == "--mode") o.mode = next();
+    else if (a == "--keep-last") o.keep_last = next() == "1";
     else {
       std::fprintf(stderr, "unknown arg %s\n", a.c_str());
       return 2;

@@ -51,7 +51,8 @@ class EngineConfigC(C.Structure):
                 ("chunk_quantum", u64), ("storage_bandwidth_Bps", f64), ("fsync_on_finalize", i32),
                 ("flush_threads", u32), ("large_leaf_threshold", u64), ("reserve_timeout_ms", i64),
                 ("device", i32), ("ce_threshold", u64), ("kernel_ctas", u32), ("group_bytes", u64),
-                ("force_kernel", i32), ("force_copy_engine", i32), ("hugepages", i32)]
+                ("force_kernel", i32), ("force_copy_engine", i32), ("hugepages", i32),
+                ("flush_discard", i32)]
 
 
 class CountersC(C.Structure):
@@ -139,6 +140,7 @@ ENGINE_SYMBOLS = [
     ("lzckpt_engine_snapshot_stats", i32, [vp, P(SnapshotStatsC)]),
     ("lzckpt_engine_flush_stats", i32, [vp, P(u64), P(u64)]),
     ("lzckpt_engine_snapshot_stream", vp, [vp]),
+    ("lzckpt_engine_set_copy_variant", i32, [vp, u64, i32, i32, u32, u64]),
     ("lzckpt_ticket_release", None, [vp]),
     ("lzckpt_ticket_id", u64, [vp]),
     ("lzckpt_ticket_step", u64, [vp]),

@@ -476,6 +476,7 @@ void lzckpt_engine_config_defaults(lzckpt_engine_config* c) {
   c->force_kernel = 0;
   c->force_copy_engine = 0;
   c->hugepages = 0;
+  c->flush_discard = 0;
 }
 
 int lzckpt_engine_create(const lzckpt_engine_config* c, const lzckpt_topology* topo, uint32_t rank_dp,
@@ -500,6 +501,7 @@ int lzckpt_engine_create(const lzckpt_engine_config* c, const lzckpt_topology* t
     cfg.snapshot.force_kernel = c->force_kernel != 0;
     cfg.snapshot.force_copy_engine = c->force_copy_engine != 0;
     cfg.pool.hugepages = c->hugepages != 0;
+    cfg.flush.discard = c->flush_discard != 0;
     auto h = std::make_unique<lzckpt_engine>();
     h->topo = to_topo(topo);
     h->e = std::make_unique<Engine>(std::move(cfg), h->topo, RankCoord{rank_dp, rank_pp, rank_tp});
@@ -593,6 +595,20 @@ int lzckpt_engine_flush_stats(const lzckpt_engine* e, uint64_t* bytes_written, u
     need(e, "engine");
     if (bytes_written) *bytes_written = e->e->flush().bytes_written();
     if (files_persisted) *files_persisted = e->e->flush().files_persisted();
+  });
+}
+
+int lzckpt_engine_set_copy_variant(lzckpt_engine* e, uint64_t ce_threshold, int force_kernel, int force_copy_engine,
+                                   uint32_t kernel_ctas, uint64_t group_bytes) {
+  return guard([&] {
+    need(e, "engine");
+    SnapshotOptions o = e->e->transfers().options();
+    o.ce_threshold = ce_threshold;
+    o.force_kernel = force_kernel != 0;
+    o.force_copy_engine = force_copy_engine != 0;
+    if (kernel_ctas) o.kernel_ctas = kernel_ctas;
+    if (group_bytes) o.group_bytes = group_bytes;
+    e->e->transfers().set_options(o);
   });
 }
 

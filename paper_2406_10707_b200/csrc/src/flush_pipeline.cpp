@@ -69,10 +69,13 @@ uint64_t FlushPipeline::register_file(std::filesystem::path path, CheckpointFile
   if (seg.length != expected) {
     throw Error("segment length does not match file payload for " + path.string());
   }
-  std::error_code ec;
-  std::filesystem::create_directories(path.parent_path(), ec);
-  const int fd = ::open(path.c_str(), O_CREAT | O_WRONLY | O_TRUNC | O_CLOEXEC, 0644);
-  if (fd < 0) throw IoError("cannot create " + path.string() + ": " + std::strerror(errno));
+  int fd = -1;
+  if (!config_.discard) {
+    std::error_code ec;
+    std::filesystem::create_directories(path.parent_path(), ec);
+    fd = ::open(path.c_str(), O_CREAT | O_WRONLY | O_TRUNC | O_CLOEXEC, 0644);
+    if (fd < 0) throw IoError("cannot create " + path.string() + ": " + std::strerror(errno));
+  }
 
   FileRecord f;
   f.path = std::move(path);
@@ -127,6 +130,11 @@ void FlushPipeline::enqueue_flush(uint64_t segment_id, uint64_t offset, uint64_t
       return;
     }
     f.enqueued += length;
+    if (config_.discard) {
+      f.accounted += length;
+      if (f.enqueued == f.expected) maybe_finalize(lk, id);
+      return;
+    }
 
     uint64_t writable = length;
     if (fail_after_ >= 0) {
@@ -281,8 +289,26 @@ void FlushPipeline::maybe_finalize(std::unique_lock<std::mutex>& lk, uint64_t id
   FileRecord& f = files_.at(id);
   if (f.finalizing || f.jobs != 0 || f.enqueued != f.expected || f.accounted != f.expected) return;
   const bool healthy = !f.abandoned;
-  if (healthy && f.entries_done != f.entries.size()) return;
+  if (healthy && !config_.discard && f.entries_done != f.entries.size()) return;
   f.finalizing = true;
+  if (config_.discard) {
+    lk.unlock();
+    std::string err;
+    try {
+      pool_.begin_flush(f.segment_id);
+    } catch (const std::exception& e) {
+      err = e.what();
+    }
+    lk.lock();
+    if (!err.empty()) {
+      fail_locked(err);
+      return;
+    }
+    f.state = healthy ? FlushFileState::Discarded : FlushFileState::Abandoned;
+    f.finalized = true;
+    release_in_order(lk);
+    return;
+  }
   std::vector<std::byte> header;
   if (healthy) header = serialize_header(f.header);  // may throw FormatError
   lk.unlock();

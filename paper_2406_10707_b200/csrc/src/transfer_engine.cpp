@@ -121,6 +121,7 @@ TransferEngine::TransferEngine(HostBufferPool& pool, ThrottledChannel channel, S
   device_ = resolve_device(opts_.device);
   opts_.device = device_;
   ck(lzk_stream_create(device_, opts_.stream_priority, &stream_), "TransferEngine: snapshot stream");
+  issuer_ = std::thread([this] { issuer_loop(); });
   worker_ = std::thread([this] { worker_loop(); });
 }
 
@@ -129,6 +130,8 @@ TransferEngine::~TransferEngine() {
     std::lock_guard lk(mu_);
     stopping_ = true;  // queued work still runs to completion
   }
+  issue_cv_.notify_all();
+  if (issuer_.joinable()) issuer_.join();
   work_cv_.notify_all();
   if (worker_.joinable()) worker_.join();
   lzk_stream_destroy(stream_);
@@ -150,6 +153,14 @@ lzk_event* TransferEngine::take_event() {
 }
 
 void TransferEngine::give_event(lzk_event* e) { free_events_.push_back(e); }  // under mu_
+
+void TransferEngine::set_options(const SnapshotOptions& o) {
+  std::lock_guard lk(opts_mu_);
+  const int dev = opts_.device, prio = opts_.stream_priority;
+  opts_ = o;
+  opts_.device = dev;
+  opts_.stream_priority = prio;
+}
 
 void TransferEngine::submit_copies(uint64_t ticket, std::vector<std::shared_ptr<CopyTask>> tasks) {
   if (tasks.empty()) {
@@ -180,9 +191,10 @@ void TransferEngine::submit_copies(uint64_t ticket, std::vector<std::shared_ptr<
     added += t->length;
   }
 
-  const bool paced = channel_.bandwidth_Bps > 0;
-  if (paced) {
+  if (channel_.bandwidth_Bps > 0) {
     Group g;
+    g.ticket = ticket;
+    g.paced = true;
     for (auto& t : tasks) g.pieces.push_back(Piece{t, 0, t->length, true});
     std::lock_guard lk(mu_);
     if (stopping_) throw Error("submit_copies: engine is shutting down");
@@ -191,82 +203,113 @@ void TransferEngine::submit_copies(uint64_t ticket, std::vector<std::shared_ptr<
     tp.device_issued = false;
     tp.tasks.insert(tp.tasks.end(), tasks.begin(), tasks.end());
     queue_.push_back(std::move(g));
+    work_cv_.notify_one();
   } else {
-    std::lock_guard order(submit_mu_);
-    {
-      std::lock_guard lk(mu_);
-      if (stopping_) throw Error("submit_copies: engine is shutting down");
-    }
     std::deque<Group> groups;
-    issue_groups(ticket, tasks, groups);
+    build_groups(tasks, groups);  // host metadata only: never blocks on the device
     std::lock_guard lk(mu_);
+    if (stopping_) throw Error("submit_copies: engine is shutting down");
     auto& tp = tickets_[ticket];
     tp.expected += tasks.size();
+    tp.unissued += groups.size();
     tp.tasks.insert(tp.tasks.end(), tasks.begin(), tasks.end());
-    tp.last_event = groups.back().done;
-    for (auto& g : groups) queue_.push_back(std::move(g));
+    for (auto& g : groups) {
+      g.ticket = ticket;
+      issue_queue_.push_back(std::move(g));
+    }
+    issue_cv_.notify_one();
   }
   bytes_submitted_.fetch_add(added);
-  work_cv_.notify_one();
 }
 
-// Cuts the tasks into quantum-sized pieces (the reference's chunk grid), packs
-// pieces into groups of ~group_bytes and issues each group's device copies on
-// the snapshot stream: one gather-kernel launch for the small-tensor pieces,
-// copy-engine DMAs for large tensors, then the group's completion event.
-void TransferEngine::issue_groups(uint64_t ticket, const std::vector<std::shared_ptr<CopyTask>>& tasks,
-                                  std::deque<Group>& out) {
-  (void)ticket;
+// Cuts tasks into quantum-sized pieces (the reference's chunk grid, which
+// fixes the announcement sequence) and packs pieces into groups of about
+// group_bytes; each region piece becomes a gather-kernel or copy-engine
+// descriptor by the size class of its tensor.
+void TransferEngine::build_groups(const std::vector<std::shared_ptr<CopyTask>>& tasks, std::deque<Group>& out) {
+  SnapshotOptions o;
+  {
+    std::lock_guard lk(opts_mu_);
+    o = opts_;
+  }
   const uint64_t quantum = std::max<uint64_t>(channel_.chunk_quantum, 1);
-  const uint64_t group_bytes = std::max<uint64_t>(opts_.group_bytes, 1);
-  std::vector<lzk_copy_desc> kdesc, cdesc;
+  const uint64_t group_bytes = std::max<uint64_t>(o.group_bytes, 1);
   std::byte* const pool_base = pool_.data();
-
   Group cur;
   uint64_t cur_bytes = 0;
-  auto close_group = [&] {
-    if (cur.pieces.empty()) return;
-    if (!kdesc.empty()) {
-      ck(lzk_gather_d2h(stream_, kdesc.data(), uint32_t(kdesc.size()), opts_.kernel_ctas),
-         "snapshot gather launch");
-    }
-    if (!cdesc.empty()) ck(lzk_ce_copy_d2h(stream_, cdesc.data(), uint32_t(cdesc.size())), "snapshot DMA");
-    cur.done = take_event();
-    ck(lzk_event_record(cur.done, stream_), "snapshot event");
-    {
-      std::lock_guard lk(mu_);
-      stats_.groups += 1;
-      stats_.kernel_launches += (kdesc.size() + 959) / 960;
-      stats_.ce_copies += cdesc.size();
-      for (const auto& d : kdesc) stats_.kernel_bytes += d.len;
-      for (const auto& d : cdesc) stats_.ce_bytes += d.len;
-    }
-    kdesc.clear();
-    cdesc.clear();
-    out.push_back(std::move(cur));
-    cur = Group{};
-    cur_bytes = 0;
-  };
-
   for (const auto& t : tasks) {
     t->state.store(CopyState::Copying);
     const Segment seg = pool_.segment_info(t->segment_id);
     std::byte* dst = pool_base + seg.offset + t->dst_offset;
-    const bool use_ce = opts_.force_copy_engine ||
-                        (!opts_.force_kernel && t->length >= opts_.ce_threshold);
+    const bool use_ce = o.force_copy_engine || (!o.force_kernel && t->length >= o.ce_threshold);
     for (uint64_t off = 0; off < t->length; off += quantum) {
       const uint64_t n = std::min(quantum, t->length - off);
       cur.pieces.push_back(Piece{t, off, n, off + n == t->length});
       if (t->source.region) {
         const auto* src = static_cast<const std::byte*>(t->source.region->device_ptr()) + t->src_offset + off;
         lzk_copy_desc d{reinterpret_cast<uint64_t>(src), reinterpret_cast<uint64_t>(dst + off), n};
-        (use_ce ? cdesc : kdesc).push_back(d);
+        (use_ce ? cur.dma : cur.kernel).push_back(d);
       }
       cur_bytes += n;
-      if (cur_bytes >= group_bytes) close_group();
+      if (cur_bytes >= group_bytes) {
+        out.push_back(std::move(cur));
+        cur = Group{};
+        cur_bytes = 0;
+      }
     }
   }
-  close_group();
+  if (!cur.pieces.empty()) out.push_back(std::move(cur));
+  for (auto& g : out) g.kernel_ctas = o.kernel_ctas;
+}
+
+// Issuer thread: device order == submission order. Blocking here (a full
+// stream queue) never reaches the trainer.
+void TransferEngine::issue(Group& g) {
+  bool ok = true;
+  if (!g.kernel.empty()) {
+    ok = lzk_gather_d2h(stream_, g.kernel.data(), uint32_t(g.kernel.size()), g.kernel_ctas) == LZK_OK;
+  }
+  if (ok && !g.dma.empty()) ok = lzk_ce_copy_d2h(stream_, g.dma.data(), uint32_t(g.dma.size())) == LZK_OK;
+  lzk_event* e = take_event();
+  if (ok) ok = lzk_event_record(e, stream_) == LZK_OK;
+  g.done = e;
+  g.issue_failed = !ok;
+}
+
+void TransferEngine::issuer_loop() {
+  for (;;) {
+    Group g;
+    {
+      std::unique_lock lk(mu_);
+      issue_cv_.wait(lk, [&] { return stopping_ || !issue_queue_.empty(); });
+      if (issue_queue_.empty()) {
+        issuer_done_ = true;
+        work_cv_.notify_all();
+        return;
+      }
+      g = std::move(issue_queue_.front());
+      issue_queue_.pop_front();
+      issuing_ = true;
+    }
+    issue(g);
+    {
+      std::lock_guard lk(mu_);
+      issuing_ = false;
+      auto& tp = tickets_[g.ticket];
+      --tp.unissued;
+      tp.last_event = g.done;
+      stats_.groups += 1;
+      stats_.kernel_launches += (g.kernel.size() + 959) / 960;
+      stats_.ce_copies += g.dma.size();
+      for (const auto& d : g.kernel) stats_.kernel_bytes += d.len;
+      for (const auto& d : g.dma) stats_.ce_bytes += d.len;
+      g.kernel.clear();
+      g.dma.clear();
+      queue_.push_back(std::move(g));
+    }
+    work_cv_.notify_one();
+    issued_cv_.notify_all();
+  }
 }
 
 void TransferEngine::worker_loop() {
@@ -274,16 +317,16 @@ void TransferEngine::worker_loop() {
     Group g;
     {
       std::unique_lock lk(mu_);
-      work_cv_.wait(lk, [&] { return stopping_ || !queue_.empty(); });
+      work_cv_.wait(lk, [&] { return !queue_.empty() || (stopping_ && issuer_done_); });
       if (queue_.empty()) return;
       g = std::move(queue_.front());
       queue_.pop_front();
       ++in_flight_;
     }
-    if (g.done) {
-      run_device_group(g);
-    } else {
+    if (g.paced) {
       run_paced_group(g);
+    } else {
+      run_device_group(g);
     }
     {
       std::lock_guard lk(mu_);
@@ -293,10 +336,13 @@ void TransferEngine::worker_loop() {
         auto& tp = tickets_[p.task->ticket];
         ++tp.completed;
         if (p.task->state.load() == CopyState::Torn) tp.torn = true;
-        if (g.done && tp.last_event == g.done) tp.last_event = nullptr;
         if (tp.completed == tp.expected) tp.tasks.clear();  // drop region references
       }
-      if (g.done) give_event(g.done);
+      if (g.done) {
+        auto& tp = tickets_[g.ticket];
+        if (tp.last_event == g.done) tp.last_event = nullptr;
+        give_event(g.done);
+      }
     }
     progress_cv_.notify_all();
   }
@@ -323,8 +369,7 @@ void TransferEngine::run_device_group(Group& g) {
                 t.source.host_blob->data() + t.src_offset + p.offset, p.length);
     blob += p.length;
   }
-  bool device_ok = lzk_event_sync(g.done) == LZK_OK;
-  std::string device_msg = device_ok ? "" : lzk_last_error();
+  const bool device_ok = !g.issue_failed && lzk_event_sync(g.done) == LZK_OK;
   std::vector<char> torn(g.pieces.size(), 0);
   {
     std::lock_guard lk(mu_);
@@ -348,7 +393,6 @@ void TransferEngine::run_device_group(Group& g) {
     bytes_delivered_.fetch_add(p.length);
     if (chunk_cb_) chunk_cb_(t.segment_id, t.dst_offset + p.offset, p.length);
   }
-  (void)device_msg;
 }
 
 // Reference-faithful paced path (transfer_engine.cpp:117-160): chunk by chunk
@@ -421,15 +465,17 @@ bool TransferEngine::ticket_complete(uint64_t ticket) const {
 
 void TransferEngine::drain() {
   std::unique_lock lk(mu_);
-  progress_cv_.wait(lk, [&] { return queue_.empty() && in_flight_ == 0; });
+  progress_cv_.wait(lk, [&] { return issue_queue_.empty() && !issuing_ && queue_.empty() && in_flight_ == 0; });
 }
 
 bool TransferEngine::fence_on_stream(uint64_t ticket, void* cuda_stream) {
-  std::lock_guard lk(mu_);
+  std::unique_lock lk(mu_);
   auto it = tickets_.find(ticket);
   if (it == tickets_.end()) return true;
   TicketProgress& tp = it->second;
   if (!tp.device_issued) return false;
+  // Normally long done by the time the trainer reaches its optimizer step.
+  issued_cv_.wait(lk, [&] { return tp.unissued == 0; });
   for (auto& t : tp.tasks) {
     const CopyState s = t->state.load();
     if (s == CopyState::Done || s == CopyState::Torn || !t->source.region) continue;

@@ -552,6 +552,7 @@ class EngineConfig:
     force_kernel: bool = False
     force_copy_engine: bool = False
     hugepages: bool = False
+    flush_discard: bool = False
 
     def _c(self) -> N.EngineConfigC:
         c = N.EngineConfigC()
@@ -678,6 +679,11 @@ class Engine:
         b, f = C.c_uint64(), C.c_uint64()
         _check(lib.lzckpt_engine_flush_stats(self._h, C.byref(b), C.byref(f)))
         return b.value, f.value
+
+    def set_copy_variant(self, ce_threshold: int = 2 << 20, force_kernel: bool = False,
+                         force_copy_engine: bool = False, kernel_ctas: int = 0, group_bytes: int = 0) -> None:
+        _check(lib.lzckpt_engine_set_copy_variant(self._h, ce_threshold, int(force_kernel), int(force_copy_engine),
+                                                  kernel_ctas, group_bytes))
 
     @property
     def snapshot_stream(self) -> int:

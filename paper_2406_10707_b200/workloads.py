@@ -16,7 +16,7 @@ from __future__ import annotations
 import dataclasses
 from typing import List, Tuple
 
-__all__ = ["Workload", "gpt2_small", "llama7b_shard", "sweep_class", "dense_model_shard"]
+__all__ = ["Workload", "gpt2_small", "llama7b_shard", "llama_layer_sample", "sweep_class", "dense_model_shard"]
 
 
 @dataclasses.dataclass
@@ -98,10 +98,25 @@ def _llama7b_tensors(layers=32, d=4096, ff=11008, vocab=32000):
     return out
 
 
-def llama7b_shard(seed: int = 7, layers: int = 32) -> Workload:
-    """C2: LLaMA-2-7B-shaped shard on one rank, 4+12 B/param (~107.8 GB)."""
-    w = _model_state("c2-llama7b", _llama7b_tensors(layers=layers), 4, layers, "splitmix64", seed)
+def llama7b_shard(seed: int = 7, layers: int = 32, vocab: int = 32000, dp: int = 1, rank: int = 0,
+                  name: str = "c2-llama7b") -> Workload:
+    """C2: LLaMA-2-7B-shaped shard on one rank, 4+12 B/param (~107.8 GB).
+
+    dp > 1 gives weak scaling: the plan is for a dp-times larger model, so
+    every rank owns exactly one C2-sized shard (files layers-*/optimizer-<rank>)."""
+    w = _model_state(name, _llama7b_tensors(layers=layers, vocab=vocab), 4, layers, "splitmix64", seed + rank)
+    if dp > 1:
+        w.param_count *= dp
+        w.topology = (dp, 1, 1, dp, 1)
+        w.rank = (rank, 0, 0)
     return w
+
+
+def llama_layer_sample(seed: int = 7, layers: int = 1) -> Workload:
+    """Bounded CPU-baseline sample of C2: `layers` LLaMA-7B decoder layers
+    with the same tensor shapes and 4+12 B/param (3.24 GB per layer)."""
+    tensors = [t for t in _llama7b_tensors(layers=layers) if t[0].startswith("layers.")]
+    return _model_state(f"c2-sample-{layers}l", tensors, 4, layers, "splitmix64", seed)
 
 
 def dense_model_shard(name: str, tensors, bpp_model: int, layers: int, seed: int) -> Workload:

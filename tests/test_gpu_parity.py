@@ -1,0 +1,403 @@
+"""GPU parity: the B200 engine's shard files against the reference's own
+output (tests/golden/ref_fixtures.json, produced by the reference engine) and
+byte-for-byte against the oracle's composition of the same workload; the
+gather/scatter kernels against numpy on random byte-granular layouts; torn
+detection, the device-side lazy fence, restore and backpressure.
+
+Everything calls through the C ABI (liblzckpt_b200.so / liblzk_cuda.so)."""
+import ctypes as C
+import os
+import shutil
+import threading
+import time
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+C1_GOLDEN = {"step-1/rank-0-0-0/layers-0-11.ckpt": (248887594, 0x18D06AB61AFAE34A),
+             "step-1/rank-0-0-0/optimizer-0.ckpt": (1493305660, 0xC1F7BF0708955268)}
+
+# engine knob sets that must all give identical files
+VARIANTS = {
+    "default": {},
+    "kernel-only": {"force_kernel": True},
+    "copy-engine-only": {"force_copy_engine": True},
+    "tiny-groups": {"group_bytes": 4096, "chunk_quantum": 1500, "kernel_ctas": 3},
+}
+
+
+@pytest.fixture(scope="module")
+def gpu(lz):
+    assert lz.device_count() > 0, "GPU tests need a CUDA device (no CPU fallback exists)"
+    return lz
+
+
+def run_capture(lz, w, thr, root, spec_dir, **knobs):
+    spec = w.write_spec(os.path.join(spec_dir, w.name + ".spec"))
+    built = lz.build_workload(spec, 0)
+    cfg = lz.EngineConfig(checkpoint_root=str(root), host_buffer_bytes=max(2 * built.bytes, 1 << 20) + (8 << 20),
+                          large_leaf_threshold=thr, fsync_on_finalize=False,
+                          **{k: v for k, v in knobs.items()})
+    eng = lz.Engine(cfg, built.topo, built.rank)
+    t = eng.capture(lz.plan_checkpoint(built.topo, built.model, built.step), built.tree, built.step)
+    eng.update_barrier(t)
+    eng.wait_persisted(t)
+    assert t.status() == "persisted" and not t.torn()
+    return eng, built, t
+
+
+@pytest.mark.parametrize("variant", list(VARIANTS))
+def test_files_match_reference_and_oracle(gpu, oracle, cases, fixtures, tmp_path, variant):
+    lz = gpu
+    for name, (w, thr) in cases.items():
+        root = tmp_path / f"{name}-{variant}"
+        eng, built, t = run_capture(lz, w, thr, root, str(tmp_path), **VARIANTS[variant])
+        want = fixtures[name]["files"]
+        expect = oracle.compose_files(w, thr)
+        got = {os.path.relpath(f, root): f for f in t.shard_files()}
+        assert set(got) == set(want) == set(expect), name
+        assert t.payload_bytes() == fixtures[name]["payload"]
+        for rel, path in got.items():
+            data = np.fromfile(path, dtype=np.uint8)
+            assert data.size == want[rel]["size"], (name, rel)
+            assert f"{oracle.fnv64(data):016x}" == want[rel]["fnv"], (name, rel)
+            assert np.array_equal(data, expect[rel]), (name, rel)
+        eng.close()
+
+
+def test_c1_golden_digests_and_restore(gpu, oracle, tmp_path):
+    lz = gpu
+    from paper_2406_10707_b200.workloads import gpt2_small
+    w = gpt2_small()
+    eng, built, t = run_capture(lz, w, 1 << 20, tmp_path / "c1", str(tmp_path))
+    got = {}
+    for f in t.shard_files():
+        data = np.fromfile(f, dtype=np.uint8)
+        got[os.path.relpath(f, tmp_path / "c1")] = (data.size, oracle.fnv64(data))
+    assert got == C1_GOLDEN
+    m = lz.ManifestStore(tmp_path / "c1" / "manifest.json")
+    m.commit_step(1, lz.committed_record(t, str(tmp_path / "c1")))
+    back = eng.restore(m, 1)
+    src = oracle.generate(w)
+    index = {p: i for i, (_, p, _) in enumerate(w.leaves)}
+    assert back.leaf_count() == len(w.leaves)
+    for leaf in back.flatten():
+        assert leaf.is_region
+        assert back.region_at(leaf.path).clone_bytes() == src[index[leaf.path]].tobytes(), leaf.path
+        assert back.region_at(leaf.path).version() == 0
+    with pytest.raises(lz.NotCommitted):
+        eng.restore(m, 99)
+    eng.close()
+
+
+# ---------------------------------------------------------------------------
+# kernels through lzk_cuda.h
+
+
+class Dev:
+    def __init__(self, lz):
+        self.d = lz.dev
+
+    def ck(self, rc):
+        if rc != 0:
+            raise RuntimeError(self.d.lzk_last_error().decode())
+
+    def pinned(self, n):
+        p = C.c_void_p()
+        self.ck(self.d.lzk_host_alloc(max(n, 1), 1, C.byref(p)))
+        arr = np.ctypeslib.as_array((C.c_uint8 * max(n, 1)).from_address(p.value))
+        return p.value, arr
+
+    def dalloc(self, n):
+        p = C.c_void_p()
+        self.ck(self.d.lzk_dev_alloc(0, max(n, 1), C.byref(p)))
+        return p.value
+
+    def stream(self):
+        s = C.c_void_p()
+        self.ck(self.d.lzk_stream_create(0, 0, C.byref(s)))
+        return s
+
+
+def descs(items):
+    from paper_2406_10707_b200 import _native as N
+    arr = (N.CopyDescC * max(len(items), 1))()
+    for i, (s, d, n) in enumerate(items):
+        arr[i] = N.CopyDescC(s, d, n)
+    return arr
+
+
+@pytest.mark.parametrize("direction", ["d2h", "h2d", "d2d"])
+def test_gather_kernel_random_layouts(gpu, direction):
+    dv = Dev(gpu)
+    rng = np.random.default_rng(17)
+    src_bytes = 24 << 20
+    dst_bytes = 112 << 20
+    host_src_p, host_src = dv.pinned(src_bytes)
+    host_dst_p, host_dst = dv.pinned(dst_bytes)
+    dsrc, ddst = dv.dalloc(src_bytes), dv.dalloc(dst_bytes)
+    host_src[:] = rng.integers(0, 256, src_bytes, dtype=np.uint8)
+    dv.ck(dv.d.lzk_memcpy_h2d(0, dsrc, host_src_p, src_bytes))
+    s = dv.stream()
+    for trial in range(6):
+        n = int(rng.integers(1, 2500))
+        sizes = rng.integers(0, 40000, n)
+        if trial == 0:
+            sizes[:5] = [0, 1, 15, 16, 17]
+        if trial == 5:
+            sizes = rng.integers(200_000, 2_000_000, 8)
+            n = len(sizes)
+        # non-overlapping destinations at arbitrary byte offsets; sources anywhere
+        gaps = rng.integers(0, 40, n)
+        doff = np.cumsum(gaps + sizes) - sizes
+        assert doff[-1] + sizes[-1] <= dst_bytes
+        soff = [int(rng.integers(0, src_bytes - z)) if z < src_bytes else 0 for z in sizes]
+        expect = np.zeros(dst_bytes, dtype=np.uint8)
+        expect[:] = 0xA5
+        ref_src = host_src
+        for z, so, do in zip(sizes, soff, doff):
+            expect[do:do + z] = ref_src[so:so + z]
+        if direction == "d2h":
+            host_dst[:] = 0xA5
+            arr = descs([(dsrc + so, host_dst_p + int(do), int(z)) for z, so, do in zip(sizes, soff, doff)])
+            dv.ck(dv.d.lzk_gather_d2h(s, arr, n, int(rng.integers(0, 20))))
+            dv.ck(dv.d.lzk_stream_sync(s))
+            got = host_dst
+        elif direction == "h2d":
+            dv.ck(dv.d.lzk_dev_memset(0, ddst, 0xA5, dst_bytes))
+            arr = descs([(host_src_p + so, ddst + int(do), int(z)) for z, so, do in zip(sizes, soff, doff)])
+            dv.ck(dv.d.lzk_scatter_h2d(s, arr, n, 0))
+            dv.ck(dv.d.lzk_stream_sync(s))
+            dv.ck(dv.d.lzk_memcpy_d2h(0, host_dst_p, ddst, dst_bytes))
+            got = host_dst
+        else:
+            dv.ck(dv.d.lzk_dev_memset(0, ddst, 0xA5, dst_bytes))
+            arr = descs([(dsrc + so, ddst + int(do), int(z)) for z, so, do in zip(sizes, soff, doff)])
+            dv.ck(dv.d.lzk_gather_d2d(s, arr, n, 0))
+            dv.ck(dv.d.lzk_stream_sync(s))
+            dv.ck(dv.d.lzk_memcpy_d2h(0, host_dst_p, ddst, dst_bytes))
+            got = host_dst
+        bad = np.nonzero(got != expect)[0]
+        assert bad.size == 0, (direction, trial, bad[:10])
+    dv.d.lzk_stream_destroy(s)
+    dv.d.lzk_dev_free(0, dsrc)
+    dv.d.lzk_dev_free(0, ddst)
+    dv.d.lzk_host_free(host_src_p)
+    dv.d.lzk_host_free(host_dst_p)
+
+
+def test_fill_kernel_matches_oracle_generator(gpu, oracle):
+    dv = Dev(gpu)
+    s = dv.stream()
+    for leaf, size in [(0, 1), (3, 7), (9, 8), (12, 4097), (77, 1 << 20)]:
+        d = dv.dalloc(size)
+        dv.ck(dv.d.lzk_fill_splitmix(s, d, size, 1234, leaf))
+        dv.ck(dv.d.lzk_stream_sync(s))
+        p, h = dv.pinned(size)
+        dv.ck(dv.d.lzk_memcpy_d2h(0, p, d, size))
+        want = np.empty(size, dtype=np.uint8)
+        oracle.L.lzo_fill_splitmix(1234, leaf, size, want.ctypes.data)
+        assert np.array_equal(h[:size], want)
+        dv.d.lzk_host_free(p)
+        dv.d.lzk_dev_free(0, d)
+    dv.d.lzk_stream_destroy(s)
+
+
+# ---------------------------------------------------------------------------
+# lazy fence semantics
+
+
+def small_engine(lz, root, **kw):
+    topo = lz.ParallelTopology(1, 1, 1, 1, 1)
+    cfg = lz.EngineConfig(checkpoint_root=str(root), host_buffer_bytes=64 << 20, large_leaf_threshold=4096,
+                          fsync_on_finalize=False, **kw)
+    return lz.Engine(cfg, topo, lz.RankCoord()), topo
+
+
+def tiny_model(lz):
+    return lz.ModelSpec(param_count=4096, layer_count=4)
+
+
+def mixed_tree(lz, rng):
+    t = lz.StateTree()
+    regs = {}
+    for path, n in [("layers/block0/w", 5000), ("layers/block1/w", 3192), ("optim/moments", 40000)]:
+        regs[path] = lz.DeviceRegion(rng.integers(0, 256, n, dtype=np.uint8).tobytes())
+        t.set_region(path, regs[path])
+    t.set_blob("optim/step", b"\x01" * 8)
+    t.set_blob("optim/extra", bytes(9144))
+    return t, regs
+
+
+def test_mutation_mid_copy_tears_and_files_stay_headerless(gpu, tmp_path):
+    """reference test_engine.cpp:183-215 through the Python/C ABI: a paced
+    channel (50 MB/s), the first shard's region mutated before the barrier."""
+    lz = gpu
+    topo = lz.ParallelTopology(1, 1, 1, 1, 1)
+    cfg = lz.EngineConfig(checkpoint_root=str(tmp_path), host_buffer_bytes=32 << 20, large_leaf_threshold=4096,
+                          fsync_on_finalize=False, copy_bandwidth_Bps=50e6, chunk_quantum=64 << 10)
+    eng = lz.Engine(cfg, topo, lz.RankCoord())
+    model = lz.ModelSpec(param_count=1 << 20, layer_count=4)
+    weights = lz.DeviceRegion(bytes(range(256)) * (8192))  # 2 MiB
+    tree = lz.StateTree()
+    tree.set_region("layers/w", weights)
+    tree.set_region("optim/m", lz.DeviceRegion(12 << 20))
+    t = eng.capture(lz.plan_checkpoint(topo, model, 5), tree, 5)
+    time.sleep(0.005)
+    weights.write(0, b"\x01")
+    with pytest.raises(lz.TornSnapshot):
+        eng.update_barrier(t)
+    assert t.torn() and t.status() == "failed" and "changed" in t.failure_reason()
+    with pytest.raises(lz.TornSnapshot):
+        eng.wait_persisted(t)
+    eng.drain()
+    for f in t.shard_files():
+        assert os.path.exists(f)
+        with pytest.raises(lz.BadMagic):
+            lz.read_header(f)
+    eng.close()
+
+
+def test_unpaced_mutation_after_barrier_is_not_torn(gpu, tmp_path):
+    lz = gpu
+    rng = np.random.default_rng(2)
+    eng, topo = small_engine(lz, tmp_path)
+    tree, regs = mixed_tree(lz, rng)
+    before = {p: r.clone_bytes() for p, r in regs.items()}
+    t = eng.capture(lz.plan_checkpoint(topo, tiny_model(lz), 6), tree, 6)
+    eng.update_barrier(t)
+    regs["optim/moments"].mutate(lambda b: b.__setitem__(slice(0, 100), bytes(100)))
+    eng.wait_persisted(t)
+    assert not t.torn()
+    h = lz.read_header(t.shard_files()[1])
+    assert lz.read_entry(t.shard_files()[1], h, "optim/moments") == before["optim/moments"]
+    eng.close()
+
+
+def test_small_leaves_are_captured_at_capture_time(gpu, tmp_path):
+    """reference test_engine.cpp:217-240: inline leaves are snapshotted
+    synchronously, so a mutation right after capture() cannot reach them."""
+    lz = gpu
+    eng, topo = small_engine(lz, tmp_path, copy_bandwidth_Bps=5e6, chunk_quantum=4096)
+    t_ = lz.StateTree()
+    small = lz.DeviceRegion(bytes(range(256)) * 4)  # 1024 B < threshold
+    big = lz.DeviceRegion(bytes(8192 - 1024))
+    t_.set_region("layers/small", small)
+    t_.set_region("layers/big", big)
+    t_.set_region("optim/m", lz.DeviceRegion(bytes(49152)))
+    t = eng.capture(lz.plan_checkpoint(topo, tiny_model(lz), 7), t_, 7)
+    small.write(0, b"\xff" * 16)  # after capture, before barrier
+    eng.update_barrier(t)
+    eng.wait_persisted(t)
+    m = lz.ManifestStore(tmp_path / "manifest.json")
+    m.commit_step(7, lz.committed_record(t, str(tmp_path)))
+    back = eng.restore(m, 7)
+    assert back.region_at("layers/small").clone_bytes() == bytes(range(256)) * 4
+    eng.close()
+
+
+def test_device_side_fence_orders_optimizer_after_snapshot(gpu, tmp_path):
+    """update_barrier_on_stream: the trainer's stream waits for the snapshot;
+    the 'optimizer step' queued after it must not leak into the checkpoint,
+    and the declared mutation (bump_version) after the fence is not a tear."""
+    lz = gpu
+    torch = pytest.importorskip("torch")
+    eng, topo = small_engine(lz, tmp_path)
+    layers = torch.arange(2048, dtype=torch.float32, device="cuda")  # 8192 B
+    optim = torch.full((12288,), 3.0, dtype=torch.float32, device="cuda")  # 49152 B
+    torch.cuda.synchronize()
+    tree = lz.StateTree()
+    rl, ro = lz.DeviceRegion.wrap(layers), lz.DeviceRegion.wrap(optim)
+    tree.set_region("layers/w", rl)
+    tree.set_region("optim/m", ro)
+    want = optim.cpu().numpy().tobytes()
+    s = torch.cuda.Stream()
+    for step in range(1, 4):
+        t = eng.capture(lz.plan_checkpoint(topo, tiny_model(lz), step), tree, step)
+        eng.update_barrier_on_stream(t, s.cuda_stream)
+        with torch.cuda.stream(s):
+            optim.add_(1.0)  # optimizer step, stream-ordered after the snapshot
+        ro.bump_version()
+        eng.wait_persisted(t)
+        assert not t.torn()
+        f = t.shard_files()[1]
+        got = lz.read_entry(f, lz.read_header(f), "optim/m")
+        assert got == want, step
+        s.synchronize()
+        want = optim.cpu().numpy().tobytes()
+    eng.close()
+
+
+def test_restore_into_existing_regions(gpu, tmp_path):
+    lz = gpu
+    rng = np.random.default_rng(4)
+    eng, topo = small_engine(lz, tmp_path)
+    tree, regs = mixed_tree(lz, rng)
+    before = {p: r.clone_bytes() for p, r in regs.items()}
+    t = eng.capture(lz.plan_checkpoint(topo, tiny_model(lz), 9), tree, 9)
+    eng.update_barrier(t)
+    eng.wait_persisted(t)
+    m = lz.ManifestStore(tmp_path / "manifest.json")
+    m.commit_step(9, lz.committed_record(t, str(tmp_path)))
+    for r in regs.values():
+        r.write(0, b"\x00" * 64)
+    v = regs["optim/moments"].version()
+    eng.restore_into(m, 9, tree)
+    for p, r in regs.items():
+        assert r.clone_bytes() == before[p]
+    assert regs["optim/moments"].version() > v
+    eng.close()
+
+
+def test_corrupt_file_is_rejected_on_restore(gpu, tmp_path):
+    lz = gpu
+    rng = np.random.default_rng(5)
+    eng, topo = small_engine(lz, tmp_path)
+    tree, _ = mixed_tree(lz, rng)
+    t = eng.capture(lz.plan_checkpoint(topo, tiny_model(lz), 3), tree, 3)
+    eng.update_barrier(t)
+    eng.wait_persisted(t)
+    m = lz.ManifestStore(tmp_path / "manifest.json")
+    m.commit_step(3, lz.committed_record(t, str(tmp_path)))
+    f = t.shard_files()[1]
+    raw = bytearray(open(f, "rb").read())
+    raw[-5] ^= 0x40
+    open(f, "wb").write(raw)
+    with pytest.raises(lz.ChecksumMismatch):
+        eng.restore(m, 3)
+    open(f, "wb").write(raw[:-1])
+    with pytest.raises(lz.TruncatedFile):
+        eng.restore(m, 3)
+    eng.close()
+
+
+def test_pool_backpressure_blocks_capture_until_flush_releases(gpu, tmp_path):
+    lz = gpu
+    rng = np.random.default_rng(6)
+    topo = lz.ParallelTopology(1, 1, 1, 1, 1)
+    # pool fits one capture (~57.5 KB payload) but not two; slow storage
+    cfg = lz.EngineConfig(checkpoint_root=str(tmp_path), host_buffer_bytes=80_000, large_leaf_threshold=4096,
+                          fsync_on_finalize=False, storage_bandwidth_Bps=1e6)
+    eng = lz.Engine(cfg, topo, lz.RankCoord())
+    tree, _ = mixed_tree(lz, rng)
+    t1 = eng.capture(lz.plan_checkpoint(topo, tiny_model(lz), 1), tree, 1)
+    eng.update_barrier(t1)
+    t0 = time.perf_counter()
+    t2 = eng.capture(lz.plan_checkpoint(topo, tiny_model(lz), 2), tree, 2)
+    waited = time.perf_counter() - t0
+    assert waited > 0.02  # blocked on t1's flush (57 KB at 1 MB/s)
+    eng.update_barrier(t2)
+    eng.wait_persisted(t2)
+    assert t1.status() == "persisted" and t2.status() == "persisted"
+    with pytest.raises(lz.SizeExceedsCapacity):
+        big = lz.StateTree()
+        big.set_region("layers/w", lz.DeviceRegion(8192))
+        big.set_region("optim/m", lz.DeviceRegion(49152))
+        small_cfg = lz.EngineConfig(checkpoint_root=str(tmp_path / "x"), host_buffer_bytes=40_000,
+                                    large_leaf_threshold=4096)
+        e2 = lz.Engine(small_cfg, topo, lz.RankCoord())
+        e2.capture(lz.plan_checkpoint(topo, tiny_model(lz), 1), big, 1)
+    eng.close()

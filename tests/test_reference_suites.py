@@ -1,0 +1,26 @@
+"""Runs the reference's OWN unit-test sources for the hot path (compiled in
+place from /root/reference/proj/tests against our include/lzckpt headers and
+liblzckpt_b200.so by tests/reftests/Makefile, with our doctest shim) on the
+GPU: transfer (D2H engine, chunk order, torn detection, pacing), flush
+(header-last, abandon, injected failure, interleaving), buffer pool
+(backpressure, timeouts), engine (round trip, inline capture, statuses,
+blocking capture), state tree, plus the host-only suites."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SUITES = ["test_transfer", "test_flush", "test_buffer_pool", "test_engine", "test_state_tree", "test_ring",
+          "test_format", "test_topology", "test_manifest"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("suite", SUITES)
+def test_reference_suite_passes(suite):
+    exe = os.path.join(ROOT, "tests", "reftests", "bin", suite)
+    assert os.path.exists(exe), f"{exe} missing: build with `make -C tests/reftests` where /root/reference exists"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    summary = r.stderr.strip().splitlines()[-1] if r.stderr.strip() else ""
+    assert r.returncode == 0, r.stderr[-4000:]
+    assert "| 0 failed |" in summary and summary.endswith(" 0 failed"), summary
