@@ -68,12 +68,16 @@ class FlushPipeline {
   size_t queue_depth() const;
 
  private:
-  struct EntryCursor {
-    uint64_t begin = 0;     // payload-relative
-    uint64_t end = 0;
-    uint64_t resident = 0;  // bytes [begin, resident) are in the pool
+  // Consecutive entries hashed by one job at a time, strictly in byte order
+  // (FNV-1a is sequential per entry); different runs hash in parallel. A run
+  // is one large entry or several small ones adding up to >= kRunBytes.
+  struct HashRun {
+    size_t first = 0, last = 0;  // entries [first, last)
+    uint64_t begin = 0, end = 0; // payload-relative byte range
+    uint64_t resident = 0;       // bytes [begin, resident) are in the pool
     uint64_t hashed = 0;
-    uint64_t state = Fnv64::kOffset;  // FNV-1a over [begin, hashed)
+    size_t cur = 0;              // entry being folded
+    uint64_t state = Fnv64::kOffset;
     bool busy = false;
   };
   struct FileRecord {
@@ -82,11 +86,15 @@ class FlushPipeline {
     uint64_t segment_id = 0;
     uint64_t header_size = 0;
     uint64_t expected = 0;
-    uint64_t enqueued = 0;   // next in-order chunk offset
-    uint64_t accounted = 0;  // written + starved bytes
-    uint32_t jobs = 0;       // outstanding jobs touching this file
+    uint64_t enqueued = 0;       // next in-order chunk offset (= resident end)
+    uint64_t write_queued = 0;   // bytes [0, write_queued) handed to writers
+    uint64_t starve_from = ~0ull;// injected failure: bytes >= this never reach the disk
+    uint64_t accounted = 0;      // written + starved bytes
+    uint32_t jobs = 0;           // outstanding jobs touching this file
+    uint32_t writes_inflight = 0;
     const std::byte* base = nullptr;
-    std::vector<EntryCursor> entries;
+    std::vector<uint64_t> entry_begin;  // payload-relative, per entry
+    std::vector<HashRun> runs;
     size_t entries_done = 0;
     int fd = -1;
     bool abandoned = false;
@@ -100,12 +108,14 @@ class FlushPipeline {
     uint64_t file = 0;
     uint64_t offset = 0;  // write: payload offset
     uint64_t length = 0;  // write: bytes
-    size_t entry = 0;     // hash: entry index
+    size_t run = 0;       // hash: run index
   };
+  static constexpr uint64_t kRunBytes = 4ull << 20;
 
+  void queue_writes(uint64_t id, FileRecord& f);
   void worker_loop();
   void run_write(FileRecord& f, const Job& j);
-  void run_hash(uint64_t file_id, size_t entry);
+  void run_hash(uint64_t file_id, size_t run);
   void maybe_finalize(std::unique_lock<std::mutex>& lk, uint64_t file_id);
   void release_in_order(std::unique_lock<std::mutex>& lk);
   void fail_locked(const std::string& why);

@@ -100,7 +100,7 @@ struct SnapshotOptions {
   int device = -1;                    // -1: current device at construction
   uint64_t ce_threshold = 2ull << 20; // tasks >= this go to the copy engines
   uint32_t kernel_ctas = 16;          // gather kernel grid (PCIe-saturating)
-  uint64_t group_bytes = 64ull << 20; // bytes per completion event
+  uint64_t group_bytes = 256ull << 20; // bytes per completion event (and max DMA size)
   int stream_priority = 1;            // > 0: below default (compute) priority
   bool force_kernel = false;          // every region chunk through the gather kernel
   bool force_copy_engine = false;     // every region chunk through the copy engines
@@ -160,6 +160,9 @@ class TransferEngine {
   // not device-issued (paced channel); the caller then waits on the host.
   bool fence_on_stream(uint64_t ticket, void* cuda_stream);
   bool ticket_complete(uint64_t ticket) const;
+  // Device time of a completed ticket's snapshot (CUDA events on the snapshot
+  // stream, first device op -> last completion); < 0 when not measured.
+  double ticket_device_ms(uint64_t ticket) const;
   const SnapshotOptions& options() const { return opts_; }
   // Changes the variant selection for subsequent submissions (device and
   // stream priority are fixed at construction).
@@ -201,6 +204,8 @@ class TransferEngine {
     bool torn = false;
     bool device_issued = true;
     lzk_event* last_event = nullptr;
+    lzk_event* start_event = nullptr;  // recorded before the ticket's first group
+    double device_ms = -1;             // first issue -> last completion, on the device
     std::vector<std::shared_ptr<CopyTask>> tasks;  // for fence versions
   };
 

@@ -250,6 +250,9 @@ uint64_t lzckpt_ticket_payload_bytes(const lzckpt_ticket* k);
 uint32_t lzckpt_ticket_file_count(const lzckpt_ticket* k);
 int lzckpt_ticket_file(const lzckpt_ticket* k, uint32_t i, char* path, uint64_t cap);
 int lzckpt_ticket_failure_reason(const lzckpt_ticket* k, char* out, uint64_t cap);
+/* Device time (ms) of the ticket's D2H snapshot, first device op to last
+ * completion on the snapshot stream; < 0 until the copies completed. */
+double lzckpt_engine_ticket_device_ms(const lzckpt_engine* e, const lzckpt_ticket* k);
 
 /* ---- synthetic workloads (tests / bench) ------------------------------------- */
 /* Materializes the spec written by paper_2406_10707_b200/workloads.py on

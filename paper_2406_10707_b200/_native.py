@@ -150,6 +150,7 @@ ENGINE_SYMBOLS = [
     ("lzckpt_ticket_file_count", u32, [vp]),
     ("lzckpt_ticket_file", i32, [vp, u32, cp, u64]),
     ("lzckpt_ticket_failure_reason", i32, [vp, cp, u64]),
+    ("lzckpt_engine_ticket_device_ms", f64, [vp, vp]),
     ("lzckpt_workload_build", i32, [cp, i32, P(vp), P(ModelSpecC), P(Topology), P(u32), P(u64), P(u64)]),
 ]
 

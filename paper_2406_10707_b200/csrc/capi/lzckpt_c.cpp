@@ -633,6 +633,10 @@ int lzckpt_ticket_file(const lzckpt_ticket* k, uint32_t i, char* path, uint64_t 
   });
 }
 
+double lzckpt_engine_ticket_device_ms(const lzckpt_engine* e, const lzckpt_ticket* k) {
+  return e && k ? e->e->transfers().ticket_device_ms(k->k->id()) : -1.0;
+}
+
 int lzckpt_ticket_failure_reason(const lzckpt_ticket* k, char* out, uint64_t cap) {
   return guard([&] {
     need(k, "ticket");

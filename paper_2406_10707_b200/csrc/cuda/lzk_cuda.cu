@@ -11,13 +11,14 @@
 //    so the call needs no staging buffer and the caller's array is free the
 //    moment the launch returns. Larger batches become several launches.
 //  * Work unit = a "tile" of <= kTile bytes of one descriptor. Tile
-//    boundaries sit at 16-byte-aligned DESTINATION addresses, so only a
+//    boundaries sit at 128-byte-aligned DESTINATION addresses, so only a
 //    descriptor's first tile has an unaligned head and only its last a tail.
 //  * Loads: aligned 128-bit LDG of the source; when source and destination
 //    disagree mod 16, each output word is funnel-shifted out of two adjacent
 //    aligned source words (the neighbour's word hits L1).
-//  * Stores: aligned 128-bit STG; a warp writes 512 contiguous bytes = four
-//    full 128-byte lines, i.e. full-size posted PCIe writes.
+//  * Stores: aligned 128-bit STG; a warp writes 512 contiguous bytes that
+//    start on a 128-byte line = four full-line posted PCIe writes (ncu showed
+//    16-byte-aligned warp stores straddling five lines cost ~15% of the link).
 //  * Grid: a handful of CTAs saturates PCIe Gen5 x16 (measured on the box:
 //    >= 4 CTAs x 256 threads reach the 52.8 GB/s SM-store plateau), so the
 //    snapshot steals ~5% of the 148 SMs from training kernels.
@@ -181,33 +182,67 @@ __device__ __forceinline__ void body_aligned(const uint4* __restrict__ sw, uint4
   }
 }
 
-// Copies n bytes src -> dst where dst + n_head is 16-byte aligned
-// (n_head < 16 bytes are copied bytewise first).
+// Aligned-destination words [w0, w1) (word j at d + 16 j), either skewed or
+// aligned source, dispatched once per span.
+__device__ __forceinline__ void copy_words(const uint8_t* s, uint4* dw, uint32_t nw) {
+  const uint32_t k = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(s) & 15u);
+  if (k == 0) {
+    body_aligned(reinterpret_cast<const uint4*>(s), dw, nw);
+    return;
+  }
+  const uint4* sa = reinterpret_cast<const uint4*>(s - k);
+  const uint32_t shift = 8u * (k & 3u);
+  switch (k >> 2) {
+    case 0: body_skewed<0>(sa, dw, nw, shift); break;
+    case 1: body_skewed<1>(sa, dw, nw, shift); break;
+    case 2: body_skewed<2>(sa, dw, nw, shift); break;
+    default: body_skewed<3>(sa, dw, nw, shift); break;
+  }
+}
+
+// Copies n bytes src -> dst. Stores are shaped for the host link: bytes up to
+// the first 16-byte boundary go bytewise, then up to seven 16-byte words up
+// to the first 128-byte line boundary, then the body, where every warp
+// stores 512 bytes starting on a line boundary (four full-line posted
+// writes, never five partial ones), then the tail.
 __device__ __forceinline__ void copy_span(const uint8_t* src, uint8_t* dst, uint64_t n) {
   uint32_t head = static_cast<uint32_t>((16u - (reinterpret_cast<uintptr_t>(dst) & 15u)) & 15u);
   if (head > n) head = static_cast<uint32_t>(n);
   if (threadIdx.x < head) dst[threadIdx.x] = src[threadIdx.x];
   const uint8_t* s = src + head;
   uint8_t* d = dst + head;
-  const uint64_t rem = n - head;
-  const uint32_t nw = static_cast<uint32_t>(rem >> 4);
-  const uint32_t tail = static_cast<uint32_t>(rem & 15u);
-  uint4* dw = reinterpret_cast<uint4*>(d);
-  const uint32_t k = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(s) & 15u);
-  if (nw) {
-    if (k == 0) {
-      body_aligned(reinterpret_cast<const uint4*>(s), dw, nw);
-    } else {
-      const uint4* sa = reinterpret_cast<const uint4*>(s - k);
-      const uint32_t shift = 8u * (k & 3u);
-      switch (k >> 2) {
-        case 0: body_skewed<0>(sa, dw, nw, shift); break;
-        case 1: body_skewed<1>(sa, dw, nw, shift); break;
-        case 2: body_skewed<2>(sa, dw, nw, shift); break;
-        default: body_skewed<3>(sa, dw, nw, shift); break;
+  uint64_t rem = n - head;
+  // 16-byte words before the first 128-byte line boundary
+  uint32_t lead = static_cast<uint32_t>(((128u - (reinterpret_cast<uintptr_t>(d) & 127u)) & 127u) >> 4);
+  if (lead > (rem >> 4)) lead = static_cast<uint32_t>(rem >> 4);
+  if (lead) {
+    // one word per thread (threads < lead), same skew handling
+    if (threadIdx.x < 32) {
+      const uint32_t k = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(s) & 15u);
+      if (threadIdx.x < lead) {
+        const uint8_t* sw = s + 16u * threadIdx.x;
+        uint4 v;
+        if (k == 0) {
+          v = ld_cached(reinterpret_cast<const uint4*>(sw));
+        } else {
+          uint32_t b[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            b[q] = uint32_t(sw[4 * q]) | (uint32_t(sw[4 * q + 1]) << 8) | (uint32_t(sw[4 * q + 2]) << 16) |
+                   (uint32_t(sw[4 * q + 3]) << 24);
+          }
+          v = make_uint4(b[0], b[1], b[2], b[3]);
+        }
+        st_word(reinterpret_cast<uint4*>(d) + threadIdx.x, v);
       }
     }
+    s += 16u * lead;
+    d += 16u * lead;
+    rem -= 16u * lead;
   }
+  const uint32_t nw = static_cast<uint32_t>(rem >> 4);
+  const uint32_t tail = static_cast<uint32_t>(rem & 15u);
+  if (nw) copy_words(s, reinterpret_cast<uint4*>(d), nw);
   if (threadIdx.x < tail) {
     const uint64_t o = static_cast<uint64_t>(nw) * 16u + threadIdx.x;
     d[o] = s[o];
@@ -224,9 +259,9 @@ __global__ void __launch_bounds__(kThreads)
       if (batch.d[mid].tile_begin <= t) lo = mid; else hi = mid - 1;
     }
     const Desc& dsc = batch.d[lo];
-    const uint64_t mis = dsc.dst & 15u;
+    const uint64_t mis = dsc.dst & 127u;
     const uint64_t local = t - dsc.tile_begin;
-    // tile boundaries at aligned destination addresses: [local*kTile - mis, ...)
+    // tile boundaries at 128-byte-aligned destination addresses: [local*kTile - mis, ...)
     const uint64_t b = local == 0 ? 0 : local * kTile - mis;
     uint64_t e = (local + 1) * kTile - mis;
     if (e > dsc.len) e = dsc.len;
@@ -252,7 +287,7 @@ int launch_gather(cudaStream_t stream, const lzk_copy_desc* d, uint32_t n, uint3
       x.dst = d[i].dst;
       x.len = d[i].len;
       x.tile_begin = tiles;
-      tiles += (d[i].len + (d[i].dst & 15u) + kTile - 1) / kTile;
+      tiles += (d[i].len + (d[i].dst & 127u) + kTile - 1) / kTile;
     }
     if (batch.n == 0) continue;
     batch.total_tiles = tiles;

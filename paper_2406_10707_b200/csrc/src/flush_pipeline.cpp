@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cerrno>
 #include <cstring>
+#include <utility>
 
 #include "lzckpt/errors.hpp"
 
@@ -85,19 +86,31 @@ uint64_t FlushPipeline::register_file(std::filesystem::path path, CheckpointFile
   f.base = pool_.segment_data(seg);
   f.fd = fd;
   f.on_done = std::move(on_done);
-  for (const auto& e : header.entries) {
-    EntryCursor c;
-    c.begin = e.offset >= header_size ? e.offset - header_size : 0;
-    c.end = c.begin + e.length;
-    c.resident = c.hashed = c.begin;
-    f.entries.push_back(c);
-  }
   f.header = std::move(header);
-  // Zero-length entries hash to the FNV basis without waiting for bytes.
-  for (size_t i = 0; i < f.entries.size(); ++i) {
-    if (f.entries[i].begin == f.entries[i].end) {
-      f.header.entries[i].checksum = Fnv64::kOffset;
+  // Hash runs over consecutive entries; zero-length entries hash to the FNV
+  // basis without waiting for bytes.
+  const auto& ents = f.header.entries;
+  f.entry_begin.reserve(ents.size());
+  for (const auto& e : ents) f.entry_begin.push_back(e.offset >= header_size ? e.offset - header_size : 0);
+  for (size_t i = 0; i < ents.size();) {
+    HashRun r;
+    r.first = r.cur = i;
+    r.begin = r.resident = r.hashed = f.entry_begin[i];
+    uint64_t bytes = 0;
+    do {
+      bytes += ents[i].length;
+      ++i;
+    } while (i < ents.size() && bytes < kRunBytes && ents[i].length < kRunBytes &&
+             f.entry_begin[i] == f.entry_begin[i - 1] + ents[i - 1].length);
+    r.last = i;
+    r.end = f.entry_begin[i - 1] + ents[i - 1].length;
+    f.runs.push_back(r);
+  }
+  for (auto& r : f.runs) {
+    while (r.cur < r.last && ents[r.cur].length == 0) {  // leading empty entries
+      f.header.entries[r.cur].checksum = Fnv64::kOffset;
       ++f.entries_done;
+      ++r.cur;
     }
   }
   std::lock_guard lk(mu_);
@@ -136,27 +149,28 @@ void FlushPipeline::enqueue_flush(uint64_t segment_id, uint64_t offset, uint64_t
       return;
     }
 
-    uint64_t writable = length;
     if (fail_after_ >= 0) {
-      writable = std::min<uint64_t>(writable, uint64_t(fail_after_));
+      const uint64_t writable = std::min<uint64_t>(length, uint64_t(fail_after_));
       fail_after_ -= int64_t(writable);
-      if (writable < length) f.abandoned = true;
+      if (writable < length) {
+        f.abandoned = true;
+        f.starve_from = std::min(f.starve_from, offset + writable);
+      }
     }
-    f.accounted += length - writable;  // starved bytes never reach the disk
-    const uint64_t piece = std::max<uint64_t>(config_.write_piece, 1);
-    for (uint64_t o = 0; o < writable; o += piece) {
-      jobs_.push_back(Job{false, id, offset + o, std::min(piece, writable - o), 0});
-      ++f.jobs;
-    }
-    // Newly resident bytes feed the entry hashers (strictly in byte order).
+    queue_writes(id, f);
+    // Newly resident bytes feed the hash runs overlapping [offset, end).
     const uint64_t end = offset + length;
-    for (size_t i = 0; i < f.entries.size(); ++i) {
-      EntryCursor& e = f.entries[i];
-      if (e.end <= offset || e.begin >= end) continue;
-      e.resident = std::max(e.resident, std::min(e.end, end));
-      if (!e.busy && e.resident > e.hashed) {
-        e.busy = true;
-        jobs_.push_back(Job{true, id, 0, 0, i});
+    size_t r = size_t(std::upper_bound(f.runs.begin(), f.runs.end(), offset,
+                                       [](uint64_t o, const HashRun& x) { return o < x.begin; }) -
+                      f.runs.begin());
+    if (r > 0) --r;
+    for (; r < f.runs.size() && f.runs[r].begin < end; ++r) {
+      HashRun& h = f.runs[r];
+      if (h.end <= offset) continue;
+      h.resident = std::max(h.resident, std::min(h.end, end));
+      if (!h.busy && h.resident > h.hashed) {
+        h.busy = true;
+        jobs_.push_back(Job{true, id, 0, 0, r});
         ++f.jobs;
       }
     }
@@ -218,7 +232,7 @@ void FlushPipeline::worker_loop() {
     ++busy_workers_;
     if (j.hash) {
       lk.unlock();
-      run_hash(j.file, j.entry);
+      run_hash(j.file, j.run);
       lk.lock();
     } else {
       FileRecord& f = files_.at(j.file);
@@ -233,6 +247,9 @@ void FlushPipeline::worker_loop() {
       if (!err.empty()) fail_locked(err);
       f.accounted += j.length;
       bytes_written_ += err.empty() ? j.length : 0;
+      --f.writes_inflight;
+      queue_writes(j.file, f);
+      work_cv_.notify_all();
     }
     FileRecord& f = files_.at(j.file);
     --f.jobs;
@@ -258,30 +275,71 @@ void FlushPipeline::run_write(FileRecord& f, const Job& j) {
   pwrite_all(f.fd, f.base + j.offset, j.length, f.header_size + j.offset, f.path);
 }
 
-// Owns entry `entry` of `file_id` (busy flag) and folds resident bytes in
-// order until it catches up with residency; the last byte closes the digest.
-void FlushPipeline::run_hash(uint64_t file_id, size_t entry) {
+// Hands the file's resident-but-unwritten bytes to the writers: full pieces
+// always, a partial piece only when no write of this file is in flight (small
+// chunks coalesce behind a running write; nothing waits for more data).
+// Bytes past an injected-failure point are accounted as starved. Under mu_.
+void FlushPipeline::queue_writes(uint64_t id, FileRecord& f) {
+  const uint64_t piece = std::max<uint64_t>(config_.write_piece, 1);
+  const uint64_t writable_end = std::min(f.enqueued, f.starve_from);
+  while (f.write_queued < writable_end) {
+    const uint64_t n = std::min(piece, writable_end - f.write_queued);
+    if (n < piece && f.writes_inflight > 0 && f.enqueued < f.expected) break;
+    jobs_.push_back(Job{false, id, f.write_queued, n, 0});
+    f.write_queued += n;
+    ++f.writes_inflight;
+    ++f.jobs;
+  }
+  if (f.enqueued > f.write_queued && f.write_queued >= f.starve_from) {
+    f.accounted += f.enqueued - f.write_queued;  // starved bytes never reach the disk
+    f.write_queued = f.enqueued;
+  }
+}
+
+// Owns hash run `run` of `file_id` (busy flag) and folds resident bytes in
+// order, entry by entry, until it catches up with residency.
+void FlushPipeline::run_hash(uint64_t file_id, size_t run) {
   std::unique_lock lk(mu_);
   FileRecord& f = files_.at(file_id);
   for (;;) {
-    EntryCursor& e = f.entries[entry];
-    if (f.abandoned) e.hashed = e.resident;  // no header will ever be written
-    const uint64_t from = e.hashed, to = e.resident;
+    HashRun& h = f.runs[run];
+    if (f.abandoned) h.hashed = h.resident;  // no header will ever be written
+    const uint64_t from = h.hashed, to = h.resident;
     if (from == to) {
-      e.busy = false;
-      if (e.hashed == e.end && !f.abandoned) {
-        f.header.entries[entry].checksum = e.state;
-        ++f.entries_done;
-      }
+      h.busy = false;
       return;
     }
-    const uint64_t state = e.state;
-    const std::byte* p = f.base + from;
+    size_t cur = h.cur;
+    uint64_t state = h.state;
+    const std::byte* base = f.base;
+    std::vector<std::pair<size_t, uint64_t>> done;  // (entry, digest) finished in this pass
     lk.unlock();
-    const uint64_t folded = Fnv64::fold(state, p, to - from);
+    uint64_t pos = from;
+    while (pos < to && cur < h.last) {
+      const uint64_t eb = f.entry_begin[cur], ee = eb + f.header.entries[cur].length;
+      const uint64_t stop = std::min(ee, to);
+      if (pos < eb) pos = eb;  // bytes between entries are written, not hashed
+      state = Fnv64::fold(state, base + pos, stop - pos);
+      pos = stop;
+      if (pos == ee) {
+        done.emplace_back(cur, state);
+        state = Fnv64::kOffset;
+        ++cur;
+        while (cur < h.last && f.header.entries[cur].length == 0) {
+          done.emplace_back(cur, Fnv64::kOffset);
+          ++cur;
+        }
+      }
+    }
     lk.lock();
-    f.entries[entry].state = folded;
-    f.entries[entry].hashed = to;
+    HashRun& h2 = f.runs[run];
+    h2.hashed = to;
+    h2.cur = cur;
+    h2.state = state;
+    if (!f.abandoned) {
+      for (auto& [e, d] : done) f.header.entries[e].checksum = d;
+      f.entries_done += done.size();
+    }
   }
 }
 
@@ -289,7 +347,7 @@ void FlushPipeline::maybe_finalize(std::unique_lock<std::mutex>& lk, uint64_t id
   FileRecord& f = files_.at(id);
   if (f.finalizing || f.jobs != 0 || f.enqueued != f.expected || f.accounted != f.expected) return;
   const bool healthy = !f.abandoned;
-  if (healthy && !config_.discard && f.entries_done != f.entries.size()) return;
+  if (healthy && !config_.discard && f.entries_done != f.header.entries.size()) return;
   f.finalizing = true;
   if (config_.discard) {
     lk.unlock();

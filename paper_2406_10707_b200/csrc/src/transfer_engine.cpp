@@ -169,6 +169,7 @@ void TransferEngine::submit_copies(uint64_t ticket, std::vector<std::shared_ptr<
     return;
   }
   uint64_t added = 0;
+  uint64_t checked_segment = 0;  // tasks of one capture share a few segments
   for (const auto& t : tasks) {
     if (!t) throw Error("submit_copies: null task");
     if (t->length == 0) throw Error("submit_copies: zero-length copy");
@@ -182,9 +183,12 @@ void TransferEngine::submit_copies(uint64_t ticket, std::vector<std::shared_ptr<
                         std::to_string(t->source.region->device()) + ", engine on " +
                         std::to_string(device_));
     }
-    if (pool_.segment_state(t->segment_id) != SegmentState::Reserved) {
-      throw IllegalTransition("submit_copies: destination segment " + std::to_string(t->segment_id) +
-                              " is not Reserved");
+    if (t->segment_id != checked_segment) {
+      if (pool_.segment_state(t->segment_id) != SegmentState::Reserved) {
+        throw IllegalTransition("submit_copies: destination segment " + std::to_string(t->segment_id) +
+                                " is not Reserved");
+      }
+      checked_segment = t->segment_id;
     }
     t->ticket = ticket;
     if (has_region) t->captured_version = t->source.region->version();
@@ -237,18 +241,24 @@ void TransferEngine::build_groups(const std::vector<std::shared_ptr<CopyTask>>& 
   std::byte* const pool_base = pool_.data();
   Group cur;
   uint64_t cur_bytes = 0;
+  Segment seg;
   for (const auto& t : tasks) {
     t->state.store(CopyState::Copying);
-    const Segment seg = pool_.segment_info(t->segment_id);
+    if (seg.id != t->segment_id) seg = pool_.segment_info(t->segment_id);
     std::byte* dst = pool_base + seg.offset + t->dst_offset;
     const bool use_ce = o.force_copy_engine || (!o.force_kernel && t->length >= o.ce_threshold);
     for (uint64_t off = 0; off < t->length; off += quantum) {
       const uint64_t n = std::min(quantum, t->length - off);
+      const bool extends = !cur.pieces.empty() && cur.pieces.back().task == t;
       cur.pieces.push_back(Piece{t, off, n, off + n == t->length});
       if (t->source.region) {
-        const auto* src = static_cast<const std::byte*>(t->source.region->device_ptr()) + t->src_offset + off;
-        lzk_copy_desc d{reinterpret_cast<uint64_t>(src), reinterpret_cast<uint64_t>(dst + off), n};
-        (use_ce ? cur.dma : cur.kernel).push_back(d);
+        auto& list = use_ce ? cur.dma : cur.kernel;
+        if (extends && !list.empty()) {
+          list.back().len += n;  // one DMA / descriptor per tensor per group
+        } else {
+          const auto* src = static_cast<const std::byte*>(t->source.region->device_ptr()) + t->src_offset + off;
+          list.push_back(lzk_copy_desc{reinterpret_cast<uint64_t>(src), reinterpret_cast<uint64_t>(dst + off), n});
+        }
       }
       cur_bytes += n;
       if (cur_bytes >= group_bytes) {
@@ -291,6 +301,19 @@ void TransferEngine::issuer_loop() {
       issue_queue_.pop_front();
       issuing_ = true;
     }
+    lzk_event* start = nullptr;
+    {
+      std::lock_guard lk(mu_);
+      if (!tickets_[g.ticket].start_event) start = reinterpret_cast<lzk_event*>(1);
+    }
+    if (start) {
+      start = take_event();
+      if (lzk_event_record(start, stream_) != LZK_OK) {
+        std::lock_guard lk(mu_);
+        give_event(start);
+        start = nullptr;
+      }
+    }
     issue(g);
     {
       std::lock_guard lk(mu_);
@@ -298,6 +321,7 @@ void TransferEngine::issuer_loop() {
       auto& tp = tickets_[g.ticket];
       --tp.unissued;
       tp.last_event = g.done;
+      if (start) tp.start_event = start;
       stats_.groups += 1;
       stats_.kernel_launches += (g.kernel.size() + 959) / 960;
       stats_.ce_copies += g.dma.size();
@@ -340,6 +364,12 @@ void TransferEngine::worker_loop() {
       }
       if (g.done) {
         auto& tp = tickets_[g.ticket];
+        if (tp.completed == tp.expected && tp.start_event && tp.unissued == 0) {
+          float ms = -1;
+          if (lzk_event_elapsed_ms(tp.start_event, g.done, &ms) == LZK_OK) tp.device_ms = ms;
+          give_event(tp.start_event);
+          tp.start_event = nullptr;
+        }
         if (tp.last_event == g.done) tp.last_event = nullptr;
         give_event(g.done);
       }
@@ -461,6 +491,12 @@ bool TransferEngine::ticket_complete(uint64_t ticket) const {
   std::lock_guard lk(mu_);
   auto it = tickets_.find(ticket);
   return it == tickets_.end() || it->second.completed == it->second.expected;
+}
+
+double TransferEngine::ticket_device_ms(uint64_t ticket) const {
+  std::lock_guard lk(mu_);
+  auto it = tickets_.find(ticket);
+  return it == tickets_.end() ? -1.0 : it->second.device_ms;
 }
 
 void TransferEngine::drain() {

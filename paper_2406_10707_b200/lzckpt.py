@@ -548,7 +548,7 @@ class EngineConfig:
     device: int = -1
     ce_threshold: int = 2 << 20
     kernel_ctas: int = 16
-    group_bytes: int = 64 << 20
+    group_bytes: int = 256 << 20
     force_kernel: bool = False
     force_copy_engine: bool = False
     hugepages: bool = False
@@ -679,6 +679,9 @@ class Engine:
         b, f = C.c_uint64(), C.c_uint64()
         _check(lib.lzckpt_engine_flush_stats(self._h, C.byref(b), C.byref(f)))
         return b.value, f.value
+
+    def ticket_device_ms(self, t: CaptureTicket) -> float:
+        return lib.lzckpt_engine_ticket_device_ms(self._h, t._h)
 
     def set_copy_variant(self, ce_threshold: int = 2 << 20, force_kernel: bool = False,
                          force_copy_engine: bool = False, kernel_ctas: int = 0, group_bytes: int = 0) -> None:
