@@ -1,0 +1,65 @@
+"""Host-side logic of the N>1 path on CPU with gloo, world size 2: each rank
+derives its own shard plan from a dp=N topology (bench.py weak scaling), the
+ranks' shard files are disjoint and together cover the whole model, every
+rank's workload matches its plan exactly, and the timing reduction is a max
+over ranks."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2406_10707_b200 as lz
+    from paper_2406_10707_b200.workloads import llama7b_shard
+    w = llama7b_shard(layers=2, vocab=1000, dp=world, rank=rank)
+    topo = lz.ParallelTopology(*w.topology)
+    plan = lz.plan_checkpoint(topo, lz.ModelSpec(param_count=w.param_count, layer_count=w.layer_count,
+                                                 bytes_per_param_model=w.bpp_model,
+                                                 bytes_per_param_optimizer=w.bpp_opt), 1)
+    mine = plan.shards(rank)
+    # the rank's tree (top-level children in name order) matches its shards
+    tops = sorted({p.split("/")[0] for _, p, _ in w.leaves})
+    sizes = [sum(s for _, p, s in w.leaves if p.split("/")[0] == t) for t in tops]
+    assert sizes == [s.size_bytes for s in mine]
+    files = [f"rank-{s.owner.dp}-{s.owner.pp}-{s.owner.tp}/{s.filename}" for s in mine]
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (files, sum(sizes)))
+    # weak-scaling timing: each rank's step time, reduced as the max
+    t = torch.tensor([1.0 + rank], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        out.put((gathered, float(t.item()), plan.total_bytes()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_plans_are_disjoint_and_complete():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    gathered, tmax, total = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    all_files = [f for files, _ in gathered for f in files]
+    assert len(all_files) == len(set(all_files)) == 2 * world
+    assert sum(b for _, b in gathered) == total
+    assert tmax == 2.0
