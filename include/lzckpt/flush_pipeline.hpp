@@ -57,6 +57,16 @@ class FlushPipeline {
 
   uint64_t register_file(std::filesystem::path path, CheckpointFileHeader header,
                          uint64_t segment_id, FileDoneCallback on_done = {});
+  // B200 extension — streaming through a pool smaller than the file: the
+  // payload arrives in consecutive segments attached as they are reserved;
+  // every segment but the last is released as soon as its bytes are written
+  // and hashed, the last one after the header (file bytes are unchanged).
+  uint64_t register_streamed_file(std::filesystem::path path, CheckpointFileHeader header,
+                                  FileDoneCallback on_done = {});
+  void attach_segment(uint64_t file_id, uint64_t segment_id, uint64_t payload_offset);
+  // Gives up on the rest of a streamed file (a capture that could not get
+  // pool space): it ends Abandoned once the attached segments drain.
+  void truncate_stream(uint64_t file_id);
   void enqueue_flush(uint64_t segment_id, uint64_t segment_offset, uint64_t length);
   void abandon(uint64_t file_id);
   void inject_failure_after(uint64_t bytes);
@@ -80,19 +90,28 @@ class FlushPipeline {
     uint64_t state = Fnv64::kOffset;
     bool busy = false;
   };
+  // One reserved ring segment holding payload bytes [off, off + len).
+  struct SubSeg {
+    uint64_t id = 0;
+    uint64_t off = 0;
+    uint64_t len = 0;
+    std::byte* base = nullptr;
+    uint64_t accounted = 0;  // written + starved bytes inside this segment
+    bool released = false;
+  };
   struct FileRecord {
     std::filesystem::path path;
     CheckpointFileHeader header;
-    uint64_t segment_id = 0;
     uint64_t header_size = 0;
     uint64_t expected = 0;
+    uint64_t attached = 0;       // payload bytes covered by attached segments
     uint64_t enqueued = 0;       // next in-order chunk offset (= resident end)
     uint64_t write_queued = 0;   // bytes [0, write_queued) handed to writers
     uint64_t starve_from = ~0ull;// injected failure: bytes >= this never reach the disk
     uint64_t accounted = 0;      // written + starved bytes
     uint32_t jobs = 0;           // outstanding jobs touching this file
     uint32_t writes_inflight = 0;
-    const std::byte* base = nullptr;
+    std::vector<SubSeg> segs;    // in payload order
     std::vector<uint64_t> entry_begin;  // payload-relative, per entry
     std::vector<HashRun> runs;
     size_t entries_done = 0;
@@ -102,6 +121,8 @@ class FlushPipeline {
     bool finalized = false;
     FlushFileState state = FlushFileState::Pending;
     FileDoneCallback on_done;
+
+    size_t seg_index(uint64_t payload_off) const;  // segment holding this byte
   };
   struct Job {
     bool hash = false;
@@ -113,8 +134,12 @@ class FlushPipeline {
   static constexpr uint64_t kRunBytes = 4ull << 20;
 
   void queue_writes(uint64_t id, FileRecord& f);
+  void account(FileRecord& f, uint64_t from, uint64_t to);
+  bool hashed_through(const FileRecord& f, uint64_t end) const;
+  uint64_t register_common(std::filesystem::path path, CheckpointFileHeader header, FileDoneCallback on_done,
+                           FileRecord& f);
   void worker_loop();
-  void run_write(FileRecord& f, const Job& j);
+  void run_write(FileRecord& f, const Job& j, const std::byte* src);
   void run_hash(uint64_t file_id, size_t run);
   void maybe_finalize(std::unique_lock<std::mutex>& lk, uint64_t file_id);
   void release_in_order(std::unique_lock<std::mutex>& lk);
@@ -127,9 +152,9 @@ class FlushPipeline {
   std::condition_variable work_cv_;
   std::condition_variable done_cv_;
   std::deque<Job> jobs_;
-  std::unordered_map<uint64_t, uint64_t> seg_to_file_;
+  std::unordered_map<uint64_t, std::pair<uint64_t, size_t>> seg_to_file_;  // segment -> (file, index)
   std::unordered_map<uint64_t, FileRecord> files_;
-  std::deque<uint64_t> release_order_;  // registration order
+  std::deque<std::pair<uint64_t, size_t>> release_order_;  // (file, segment index) in reservation order
   uint64_t next_file_ = 1;
   uint64_t pending_files_ = 0;
   uint32_t callbacks_in_flight_ = 0;

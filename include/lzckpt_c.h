@@ -194,6 +194,7 @@ typedef struct lzckpt_engine_config {
   int force_copy_engine;
   int hugepages;
   int flush_discard;          /* host-memory tier only (no files) */
+  uint64_t stream_segment_bytes; /* > 0: files stream through the pool in segments this large */
 } lzckpt_engine_config;
 void lzckpt_engine_config_defaults(lzckpt_engine_config* c);
 

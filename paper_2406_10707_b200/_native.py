@@ -52,7 +52,7 @@ class EngineConfigC(C.Structure):
                 ("flush_threads", u32), ("large_leaf_threshold", u64), ("reserve_timeout_ms", i64),
                 ("device", i32), ("ce_threshold", u64), ("kernel_ctas", u32), ("group_bytes", u64),
                 ("force_kernel", i32), ("force_copy_engine", i32), ("hugepages", i32),
-                ("flush_discard", i32)]
+                ("flush_discard", i32), ("stream_segment_bytes", u64)]
 
 
 class CountersC(C.Structure):

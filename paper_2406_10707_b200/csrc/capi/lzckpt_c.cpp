@@ -477,6 +477,7 @@ void lzckpt_engine_config_defaults(lzckpt_engine_config* c) {
   c->force_copy_engine = 0;
   c->hugepages = 0;
   c->flush_discard = 0;
+  c->stream_segment_bytes = 0;
 }
 
 int lzckpt_engine_create(const lzckpt_engine_config* c, const lzckpt_topology* topo, uint32_t rank_dp,
@@ -502,6 +503,7 @@ int lzckpt_engine_create(const lzckpt_engine_config* c, const lzckpt_topology* t
     cfg.snapshot.force_copy_engine = c->force_copy_engine != 0;
     cfg.pool.hugepages = c->hugepages != 0;
     cfg.flush.discard = c->flush_discard != 0;
+    cfg.stream_segment_bytes = c->stream_segment_bytes;
     auto h = std::make_unique<lzckpt_engine>();
     h->topo = to_topo(topo);
     h->e = std::make_unique<Engine>(std::move(cfg), h->topo, RankCoord{rank_dp, rank_pp, rank_tp});

@@ -172,6 +172,12 @@ Engine::Engine(EngineConfig config, ParallelTopology topo, RankCoord rank)
     flush_.enqueue_flush(seg, off, len);
   });
   transfers_.set_torn_callback([this](const CopyTask& t) { on_torn(t.ticket); });
+  if (config_.stream_segment_bytes > 0) {
+    if (config_.stream_segment_bytes > config_.host_buffer_bytes) {
+      throw ConfigError("stream_segment_bytes exceeds the host buffer pool");
+    }
+    streamer_ = std::thread([this] { streamer_loop(); });
+  }
 }
 
 Engine::~Engine() {
@@ -179,6 +185,12 @@ Engine::~Engine() {
     drain();
   } catch (...) {
   }
+  {
+    std::lock_guard lk(stream_mu_);
+    stream_stop_ = true;
+  }
+  stream_cv_.notify_all();
+  if (streamer_.joinable()) streamer_.join();
   {
     std::lock_guard lk(mu_);
     for (auto& [id, weak] : tickets_) {
@@ -313,6 +325,81 @@ std::shared_ptr<CaptureTicket> Engine::capture(const CheckpointPlan& plan, const
 
   uint64_t total = 0;
   std::weak_ptr<CaptureTicket> weak = ticket;
+  if (config_.stream_segment_bytes > 0) {
+    // Streaming: cut each file's payload [meta][large...] into segments of at
+    // most S bytes; the streamer reserves them in order (backpressure) and
+    // submits their copies. File bytes are identical to the one-segment path.
+    const uint64_t S = config_.stream_segment_bytes;
+    std::vector<StreamJob> jobs;
+    for (auto& b : builds) {
+      const uint64_t file_id = flush_.register_streamed_file(b.path, b.header,
+                                                             [this, weak](uint64_t, FlushFileState st) {
+                                                               if (auto t = weak.lock()) on_file_done(t, st);
+                                                             });
+      {
+        std::lock_guard tl(ticket->mu_);
+        ticket->files_.push_back({b.path, file_id, 0});
+        ticket->streamed_ = true;
+      }
+      struct Src {
+        StateTree::RegionPtr region;
+        StateTree::BlobPtr blob;
+        uint64_t size;
+      };
+      std::vector<Src> srcs{{nullptr, b.meta, b.meta->size()}};
+      for (const auto& l : b.larges) srcs.push_back({l.region, l.blob, l.size});
+      size_t si = 0;
+      uint64_t soff = 0;
+      for (uint64_t seg_off = 0; seg_off < b.payload; seg_off += S) {
+        StreamJob j;
+        j.ticket = ticket;
+        j.file_id = file_id;
+        j.payload_offset = seg_off;
+        j.length = std::min(S, b.payload - seg_off);
+        for (uint64_t filled = 0; filled < j.length;) {
+          const Src& src = srcs[si];
+          const uint64_t n = std::min(src.size - soff, j.length - filled);
+          if (n) {
+            auto t = std::make_shared<CopyTask>();
+            t->ticket = ticket->id_;
+            t->shard_id = b.shard->shard_id;
+            t->source.region = src.region;
+            t->source.host_blob = src.region ? nullptr : src.blob;
+            t->src_offset = soff;
+            t->length = n;
+            t->dst_offset = filled;
+            j.tasks.push_back(std::move(t));
+          }
+          filled += n;
+          soff += n;
+          if (soff == src.size) {
+            ++si;
+            soff = 0;
+          }
+        }
+        j.tasks.back()->final_for_segment = true;
+        jobs.push_back(std::move(j));
+      }
+      total += b.payload;
+    }
+    {
+      std::lock_guard tl(ticket->mu_);
+      ticket->streams_pending_ += jobs.size();
+    }
+    {
+      std::lock_guard sl(stream_mu_);
+      for (auto& j : jobs) stream_queue_.push_back(std::move(j));
+    }
+    stream_cv_.notify_all();
+    ticket->payload_bytes_ = total;
+    const double dt = since(t0);
+    std::lock_guard lk(mu_);
+    ++counters_.captures;
+    counters_.bytes_captured += total;
+    counters_.capture_seconds += dt;
+    counters_.last_capture_seconds = dt;
+    return ticket;
+  }
   for (auto& b : builds) {
     const Segment seg = pool_.reserve(b.payload, ticket->id_);  // backpressure blocks here
     const uint64_t file_id = flush_.register_file(b.path, b.header, seg.id,
@@ -361,6 +448,68 @@ std::shared_ptr<CaptureTicket> Engine::capture(const CheckpointPlan& plan, const
   return ticket;
 }
 
+// Streamer thread: reserves each streamed segment in capture order (blocking
+// on pool backpressure, i.e. on the flush draining earlier segments),
+// attaches it to its file and submits its copies.
+void Engine::streamer_loop() {
+  for (;;) {
+    StreamJob j;
+    {
+      std::unique_lock sl(stream_mu_);
+      stream_cv_.wait(sl, [&] { return stream_stop_ || !stream_queue_.empty(); });
+      if (stream_queue_.empty()) return;
+      j = std::move(stream_queue_.front());
+      stream_queue_.pop_front();
+      stream_busy_ = true;
+    }
+    bool skip;
+    {
+      std::lock_guard tl(j.ticket->mu_);
+      skip = !j.ticket->stream_error_.empty();
+    }
+    std::string err;
+    if (!skip) {
+      try {
+        const Segment seg = pool_.reserve(j.length, j.ticket->id_);
+        flush_.attach_segment(j.file_id, seg.id, j.payload_offset);
+        for (auto& t : j.tasks) t->segment_id = seg.id;
+        transfers_.submit_copies(j.ticket->id_, std::move(j.tasks));
+      } catch (const std::exception& e) {
+        err = e.what();
+      }
+    }
+    if (!err.empty()) {
+      // Give up on the rest of this capture: its files end Abandoned once
+      // the segments already attached drain.
+      std::vector<uint64_t> ids;
+      {
+        std::lock_guard tl(j.ticket->mu_);
+        j.ticket->stream_error_ = err;
+        j.ticket->failed_ = true;
+        if (j.ticket->failure_reason_.empty()) j.ticket->failure_reason_ = "streaming capture: " + err;
+        for (const auto& f : j.ticket->files_) ids.push_back(f.flush_file_id);
+      }
+      for (uint64_t id : ids) flush_.truncate_stream(id);
+    }
+    {
+      std::lock_guard tl(j.ticket->mu_);
+      --j.ticket->streams_pending_;
+    }
+    j.ticket->done_cv_.notify_all();
+    {
+      std::lock_guard sl(stream_mu_);
+      stream_busy_ = false;
+    }
+    stream_cv_.notify_all();
+  }
+}
+
+void Engine::wait_streamed(const std::shared_ptr<CaptureTicket>& ticket) {
+  std::unique_lock tl(ticket->mu_);
+  ticket->done_cv_.wait(tl, [&] { return ticket->streams_pending_ == 0; });
+  if (!ticket->stream_error_.empty()) throw Error("streaming capture failed: " + ticket->stream_error_);
+}
+
 void Engine::update_barrier(const std::shared_ptr<CaptureTicket>& ticket) {
   const auto t0 = std::chrono::steady_clock::now();
   auto record = [&] {
@@ -370,6 +519,7 @@ void Engine::update_barrier(const std::shared_ptr<CaptureTicket>& ticket) {
     counters_.last_barrier_seconds = dt;
   };
   try {
+    wait_streamed(ticket);
     transfers_.wait_pending(ticket->id_);
   } catch (...) {
     record();
@@ -384,6 +534,7 @@ void Engine::update_barrier(const std::shared_ptr<CaptureTicket>& ticket) {
 
 void Engine::update_barrier_on_stream(const std::shared_ptr<CaptureTicket>& ticket, void* cuda_stream) {
   const auto t0 = std::chrono::steady_clock::now();
+  wait_streamed(ticket);  // streamed segments must all be on the device first
   if (!transfers_.fence_on_stream(ticket->id_, cuda_stream)) {
     update_barrier(ticket);  // paced channel: copies are host-driven
     return;
@@ -406,6 +557,10 @@ void Engine::wait_persisted(const std::shared_ptr<CaptureTicket>& ticket) {
 }
 
 void Engine::drain() {
+  {
+    std::unique_lock sl(stream_mu_);
+    stream_cv_.wait(sl, [&] { return stream_queue_.empty() && !stream_busy_; });
+  }
   transfers_.drain();
   flush_.drain();
 }
@@ -448,6 +603,10 @@ void Engine::on_torn(uint64_t ticket_id) {
 TicketStatus Engine::ticket_status(const CaptureTicket& t) const {
   if (t.failed_) return TicketStatus::Failed;
   if (t.files_done_ == t.files_.size()) return TicketStatus::Persisted;
+  if (t.streamed_) {
+    return t.streams_pending_ == 0 && transfers_.ticket_complete(t.id_) ? TicketStatus::HostResident
+                                                                         : TicketStatus::InFlight;
+  }
   for (const auto& f : t.files_) {
     try {
       if (pool_.segment_state(f.segment_id) == SegmentState::Reserved) return TicketStatus::InFlight;

@@ -9,9 +9,10 @@
 //   affected files end Abandoned, segments still release                 :197-202
 //   finalize: begin_flush, header last, fsync, close, release, callback  :243-263
 //   drain: until no pending files/jobs/callbacks or a worker fault        :104-115
-// Changed: the mutex is never held across pwrite or hashing; pwrites of
-// different pieces and hashes of different entries run on a thread pool;
-// segments are released strictly in registration (= reservation) order.
+// Changed: the mutex is never held across pwrite or hashing; a thread pool
+// pwrites coalesced pieces and hashes runs of entries in parallel (each
+// entry still folded strictly in byte order); segments are released strictly
+// in reservation order; a file may stream through several segments.
 #include "lzckpt/flush_pipeline.hpp"
 
 #include <fcntl.h>
@@ -43,6 +44,13 @@ void pwrite_all(int fd, const std::byte* p, uint64_t n, uint64_t off, const std:
 
 }  // namespace
 
+size_t FlushPipeline::FileRecord::seg_index(uint64_t payload_off) const {
+  size_t i = size_t(std::upper_bound(segs.begin(), segs.end(), payload_off,
+                                     [](uint64_t o, const SubSeg& s) { return o < s.off; }) -
+                    segs.begin());
+  return i ? i - 1 : 0;
+}
+
 FlushPipeline::FlushPipeline(HostBufferPool& pool, FlushConfig config) : pool_(pool), config_(config) {
   unsigned n = config_.threads;
   if (n == 0) n = std::clamp(std::thread::hardware_concurrency() / 2, 2u, 8u);
@@ -61,30 +69,21 @@ FlushPipeline::~FlushPipeline() {
   }
 }
 
-uint64_t FlushPipeline::register_file(std::filesystem::path path, CheckpointFileHeader header,
-                                      uint64_t segment_id, FileDoneCallback on_done) {
+// Shared by both registration flavours: validates, opens the file, builds
+// the hash runs, and inserts the record (returns its id).
+uint64_t FlushPipeline::register_common(std::filesystem::path path, CheckpointFileHeader header,
+                                        FileDoneCallback on_done, FileRecord& f) {
   const uint64_t header_size = header.serialized_size();
-  const uint64_t expected = header.payload_end() - header_size;
-  if (expected == 0) throw Error("flush file with empty payload: " + path.string());
-  const Segment seg = pool_.segment_info(segment_id);
-  if (seg.length != expected) {
-    throw Error("segment length does not match file payload for " + path.string());
-  }
-  int fd = -1;
+  f.header_size = header_size;
+  f.expected = header.payload_end() - header_size;
+  if (f.expected == 0) throw Error("flush file with empty payload: " + path.string());
   if (!config_.discard) {
     std::error_code ec;
     std::filesystem::create_directories(path.parent_path(), ec);
-    fd = ::open(path.c_str(), O_CREAT | O_WRONLY | O_TRUNC | O_CLOEXEC, 0644);
-    if (fd < 0) throw IoError("cannot create " + path.string() + ": " + std::strerror(errno));
+    f.fd = ::open(path.c_str(), O_CREAT | O_WRONLY | O_TRUNC | O_CLOEXEC, 0644);
+    if (f.fd < 0) throw IoError("cannot create " + path.string() + ": " + std::strerror(errno));
   }
-
-  FileRecord f;
   f.path = std::move(path);
-  f.segment_id = segment_id;
-  f.header_size = header_size;
-  f.expected = expected;
-  f.base = pool_.segment_data(seg);
-  f.fd = fd;
   f.on_done = std::move(on_done);
   f.header = std::move(header);
   // Hash runs over consecutive entries; zero-length entries hash to the FNV
@@ -107,7 +106,7 @@ uint64_t FlushPipeline::register_file(std::filesystem::path path, CheckpointFile
     f.runs.push_back(r);
   }
   for (auto& r : f.runs) {
-    while (r.cur < r.last && ents[r.cur].length == 0) {  // leading empty entries
+    while (r.cur < r.last && ents[r.cur].length == 0) {
       f.header.entries[r.cur].checksum = Fnv64::kOffset;
       ++f.entries_done;
       ++r.cur;
@@ -115,11 +114,77 @@ uint64_t FlushPipeline::register_file(std::filesystem::path path, CheckpointFile
   }
   std::lock_guard lk(mu_);
   const uint64_t id = next_file_++;
+  const uint64_t seg0 = f.segs.empty() ? 0 : f.segs[0].id;
   files_.emplace(id, std::move(f));
-  seg_to_file_.emplace(segment_id, id);
-  release_order_.push_back(id);
+  if (seg0) {
+    seg_to_file_.emplace(seg0, std::make_pair(id, size_t(0)));
+    release_order_.emplace_back(id, 0);
+  }
   ++pending_files_;
   return id;
+}
+
+uint64_t FlushPipeline::register_file(std::filesystem::path path, CheckpointFileHeader header,
+                                      uint64_t segment_id, FileDoneCallback on_done) {
+  const uint64_t expected = header.payload_end() - header.serialized_size();
+  if (expected == 0) throw Error("flush file with empty payload: " + path.string());
+  const Segment seg = pool_.segment_info(segment_id);
+  if (seg.length != expected) {
+    throw Error("segment length does not match file payload for " + path.string());
+  }
+  FileRecord f;
+  f.segs.push_back(SubSeg{segment_id, 0, expected, pool_.segment_data(seg), 0, false});
+  f.attached = expected;
+  return register_common(std::move(path), std::move(header), std::move(on_done), f);
+}
+
+uint64_t FlushPipeline::register_streamed_file(std::filesystem::path path, CheckpointFileHeader header,
+                                               FileDoneCallback on_done) {
+  FileRecord f;
+  return register_common(std::move(path), std::move(header), std::move(on_done), f);
+}
+
+void FlushPipeline::attach_segment(uint64_t file_id, uint64_t segment_id, uint64_t payload_offset) {
+  const Segment seg = pool_.segment_info(segment_id);
+  std::lock_guard lk(mu_);
+  auto it = files_.find(file_id);
+  if (it == files_.end()) throw Error("attach_segment: unknown flush file");
+  FileRecord& f = it->second;
+  if (payload_offset != f.attached || payload_offset + seg.length > f.expected) {
+    throw Error("attach_segment: segments must tile the payload in order for " + f.path.string());
+  }
+  f.segs.push_back(SubSeg{segment_id, payload_offset, seg.length, pool_.segment_data(seg), 0, false});
+  f.attached += seg.length;
+  seg_to_file_.emplace(segment_id, std::make_pair(file_id, f.segs.size() - 1));
+  release_order_.emplace_back(file_id, f.segs.size() - 1);
+}
+
+void FlushPipeline::truncate_stream(uint64_t file_id) {
+  std::unique_lock lk(mu_);
+  auto it = files_.find(file_id);
+  if (it == files_.end()) throw Error("truncate_stream: unknown flush file");
+  FileRecord& f = it->second;
+  f.abandoned = true;
+  f.expected = f.attached;
+  if (f.segs.empty()) {  // nothing ever attached: done right away
+    if (f.fd >= 0) ::close(f.fd);
+    f.fd = -1;
+    f.finalizing = f.finalized = true;
+    f.state = FlushFileState::Abandoned;
+    --pending_files_;
+    auto cb = f.on_done;
+    if (cb) {
+      ++callbacks_in_flight_;
+      lk.unlock();
+      cb(file_id, FlushFileState::Abandoned);
+      lk.lock();
+      --callbacks_in_flight_;
+    }
+    done_cv_.notify_all();
+    return;
+  }
+  if (f.jobs == 0) maybe_finalize(lk, file_id);
+  release_in_order(lk);
 }
 
 void FlushPipeline::fail_locked(const std::string& why) {
@@ -127,7 +192,18 @@ void FlushPipeline::fail_locked(const std::string& why) {
   done_cv_.notify_all();
 }
 
-void FlushPipeline::enqueue_flush(uint64_t segment_id, uint64_t offset, uint64_t length) {
+// Credits bytes [from, to) of the payload to their segments (under mu_).
+void FlushPipeline::account(FileRecord& f, uint64_t from, uint64_t to) {
+  f.accounted += to - from;
+  for (size_t k = f.seg_index(from); k < f.segs.size() && from < to; ++k) {
+    SubSeg& s = f.segs[k];
+    const uint64_t e = std::min(to, s.off + s.len);
+    if (e > from) s.accounted += e - from;
+    from = e;
+  }
+}
+
+void FlushPipeline::enqueue_flush(uint64_t segment_id, uint64_t seg_offset, uint64_t length) {
   {
     std::unique_lock lk(mu_);
     if (!error_.empty()) return;
@@ -136,16 +212,19 @@ void FlushPipeline::enqueue_flush(uint64_t segment_id, uint64_t offset, uint64_t
       fail_locked("chunk for unregistered segment " + std::to_string(segment_id));
       return;
     }
-    const uint64_t id = sit->second;
+    const uint64_t id = sit->second.first;
     FileRecord& f = files_.at(id);
-    if (offset != f.enqueued || offset + length > f.expected) {
+    const SubSeg& sg = f.segs[sit->second.second];
+    const uint64_t offset = sg.off + seg_offset;
+    if (offset != f.enqueued || seg_offset + length > sg.len) {
       fail_locked("out-of-order chunk for " + f.path.string());
       return;
     }
     f.enqueued += length;
     if (config_.discard) {
-      f.accounted += length;
+      account(f, offset, offset + length);
       if (f.enqueued == f.expected) maybe_finalize(lk, id);
+      release_in_order(lk);
       return;
     }
 
@@ -175,6 +254,7 @@ void FlushPipeline::enqueue_flush(uint64_t segment_id, uint64_t offset, uint64_t
       }
     }
     if (f.jobs == 0) maybe_finalize(lk, id);
+    release_in_order(lk);
   }
   work_cv_.notify_all();
 }
@@ -230,36 +310,38 @@ void FlushPipeline::worker_loop() {
     Job j = jobs_.front();
     jobs_.pop_front();
     ++busy_workers_;
+    FileRecord& f = files_.at(j.file);
     if (j.hash) {
       lk.unlock();
       run_hash(j.file, j.run);
       lk.lock();
     } else {
-      FileRecord& f = files_.at(j.file);
+      const SubSeg& s = f.segs[f.seg_index(j.offset)];  // a write never crosses segments
+      const std::byte* src = s.base + (j.offset - s.off);
       lk.unlock();
       std::string err;
       try {
-        run_write(f, j);
+        run_write(f, j, src);
       } catch (const std::exception& e) {
         err = e.what();
       }
       lk.lock();
       if (!err.empty()) fail_locked(err);
-      f.accounted += j.length;
+      account(f, j.offset, j.offset + j.length);
       bytes_written_ += err.empty() ? j.length : 0;
       --f.writes_inflight;
       queue_writes(j.file, f);
       work_cv_.notify_all();
     }
-    FileRecord& f = files_.at(j.file);
     --f.jobs;
     --busy_workers_;
     maybe_finalize(lk, j.file);
+    release_in_order(lk);
     done_cv_.notify_all();
   }
 }
 
-void FlushPipeline::run_write(FileRecord& f, const Job& j) {
+void FlushPipeline::run_write(FileRecord& f, const Job& j, const std::byte* src) {
   if (config_.storage_bandwidth_Bps > 0) {
     std::chrono::steady_clock::time_point until;
     {
@@ -272,26 +354,30 @@ void FlushPipeline::run_write(FileRecord& f, const Job& j) {
     }
     std::this_thread::sleep_until(until);
   }
-  pwrite_all(f.fd, f.base + j.offset, j.length, f.header_size + j.offset, f.path);
+  pwrite_all(f.fd, src, j.length, f.header_size + j.offset, f.path);
 }
 
 // Hands the file's resident-but-unwritten bytes to the writers: full pieces
-// always, a partial piece only when no write of this file is in flight (small
-// chunks coalesce behind a running write; nothing waits for more data).
-// Bytes past an injected-failure point are accounted as starved. Under mu_.
+// always, a partial piece only when no write of this file is in flight or it
+// completes a segment (small chunks coalesce behind a running write; nothing
+// waits for more data). Pieces never cross a segment boundary. Bytes past an
+// injected-failure point are accounted as starved. Under mu_.
 void FlushPipeline::queue_writes(uint64_t id, FileRecord& f) {
   const uint64_t piece = std::max<uint64_t>(config_.write_piece, 1);
   const uint64_t writable_end = std::min(f.enqueued, f.starve_from);
   while (f.write_queued < writable_end) {
-    const uint64_t n = std::min(piece, writable_end - f.write_queued);
-    if (n < piece && f.writes_inflight > 0 && f.enqueued < f.expected) break;
+    const SubSeg& s = f.segs[f.seg_index(f.write_queued)];
+    const uint64_t stop = std::min(writable_end, s.off + s.len);
+    const uint64_t n = std::min(piece, stop - f.write_queued);
+    const bool segment_complete = f.write_queued + n == s.off + s.len;
+    if (n < piece && !segment_complete && f.writes_inflight > 0 && f.enqueued < f.expected) break;
     jobs_.push_back(Job{false, id, f.write_queued, n, 0});
     f.write_queued += n;
     ++f.writes_inflight;
     ++f.jobs;
   }
   if (f.enqueued > f.write_queued && f.write_queued >= f.starve_from) {
-    f.accounted += f.enqueued - f.write_queued;  // starved bytes never reach the disk
+    account(f, f.write_queued, f.enqueued);  // starved bytes never reach the disk
     f.write_queued = f.enqueued;
   }
 }
@@ -311,16 +397,27 @@ void FlushPipeline::run_hash(uint64_t file_id, size_t run) {
     }
     size_t cur = h.cur;
     uint64_t state = h.state;
-    const std::byte* base = f.base;
+    // (payload start, address) of every segment the resident range touches;
+    // a segment is not released before this run has hashed through it
+    std::vector<std::pair<uint64_t, const std::byte*>> spans;
+    for (size_t k = f.seg_index(from); k < f.segs.size() && f.segs[k].off < to; ++k) {
+      spans.emplace_back(f.segs[k].off, f.segs[k].base);
+    }
     std::vector<std::pair<size_t, uint64_t>> done;  // (entry, digest) finished in this pass
     lk.unlock();
+    size_t si = 0;
     uint64_t pos = from;
     while (pos < to && cur < h.last) {
       const uint64_t eb = f.entry_begin[cur], ee = eb + f.header.entries[cur].length;
       const uint64_t stop = std::min(ee, to);
       if (pos < eb) pos = eb;  // bytes between entries are written, not hashed
-      state = Fnv64::fold(state, base + pos, stop - pos);
-      pos = stop;
+      while (pos < stop) {
+        while (si + 1 < spans.size() && spans[si + 1].first <= pos) ++si;
+        const uint64_t seg_end = si + 1 < spans.size() ? spans[si + 1].first : ~0ull;
+        const uint64_t n = std::min(seg_end, stop) - pos;
+        state = Fnv64::fold(state, spans[si].second + (pos - spans[si].first), n);
+        pos += n;
+      }
       if (pos == ee) {
         done.emplace_back(cur, state);
         state = Fnv64::kOffset;
@@ -343,70 +440,81 @@ void FlushPipeline::run_hash(uint64_t file_id, size_t run) {
   }
 }
 
+// True when every hash run has consumed all of its bytes below `end`.
+bool FlushPipeline::hashed_through(const FileRecord& f, uint64_t end) const {
+  if (config_.discard || f.abandoned) return true;
+  for (const auto& r : f.runs) {
+    if (r.begin >= end) break;
+    if (r.hashed < std::min(r.end, end)) return false;
+  }
+  return true;
+}
+
 void FlushPipeline::maybe_finalize(std::unique_lock<std::mutex>& lk, uint64_t id) {
   FileRecord& f = files_.at(id);
   if (f.finalizing || f.jobs != 0 || f.enqueued != f.expected || f.accounted != f.expected) return;
   const bool healthy = !f.abandoned;
   if (healthy && !config_.discard && f.entries_done != f.header.entries.size()) return;
   f.finalizing = true;
-  if (config_.discard) {
-    lk.unlock();
-    std::string err;
+  const uint64_t last_seg = f.segs.back().id;
+  std::vector<std::byte> header;
+  std::string err;
+  if (healthy && !config_.discard) {
     try {
-      pool_.begin_flush(f.segment_id);
+      header = serialize_header(f.header);
     } catch (const std::exception& e) {
       err = e.what();
     }
-    lk.lock();
-    if (!err.empty()) {
-      fail_locked(err);
-      return;
-    }
-    f.state = healthy ? FlushFileState::Discarded : FlushFileState::Abandoned;
-    f.finalized = true;
-    release_in_order(lk);
-    return;
   }
-  std::vector<std::byte> header;
-  if (healthy) header = serialize_header(f.header);  // may throw FormatError
   lk.unlock();
-  std::string err;
-  try {
-    pool_.begin_flush(f.segment_id);  // Filled -> Flushing
-    if (healthy) {
-      pwrite_all(f.fd, header.data(), header.size(), 0, f.path);  // header last
-      if (config_.fsync_on_finalize) ::fsync(f.fd);
+  if (err.empty()) {
+    try {
+      pool_.begin_flush(last_seg);  // Filled -> Flushing
+      if (healthy && !config_.discard) {
+        pwrite_all(f.fd, header.data(), header.size(), 0, f.path);  // header last
+        if (config_.fsync_on_finalize) ::fsync(f.fd);
+      }
+    } catch (const std::exception& e) {
+      err = e.what();
     }
-  } catch (const std::exception& e) {
-    err = e.what();
   }
-  ::close(f.fd);
+  if (f.fd >= 0) ::close(f.fd);
   lk.lock();
   f.fd = -1;
   if (!err.empty()) {
     fail_locked(err);
     return;
   }
-  f.state = healthy ? FlushFileState::Persisted : FlushFileState::Abandoned;
-  if (healthy) ++files_persisted_;
+  if (config_.discard) {
+    f.state = healthy ? FlushFileState::Discarded : FlushFileState::Abandoned;
+  } else {
+    f.state = healthy ? FlushFileState::Persisted : FlushFileState::Abandoned;
+    if (healthy) ++files_persisted_;
+  }
   f.finalized = true;
-  release_in_order(lk);
 }
 
-// Segments go back to the ring strictly in registration order (the ring only
-// frees its oldest segment); completion callbacks run outside the lock.
+// Segments go back to the ring strictly in reservation order (the ring only
+// frees its oldest segment). A file's last segment waits for the header; the
+// others leave as soon as their bytes are written and hashed (streaming).
+// The file's completion callback runs after its last segment, outside the lock.
 void FlushPipeline::release_in_order(std::unique_lock<std::mutex>& lk) {
   while (!release_order_.empty()) {
-    const uint64_t id = release_order_.front();
+    const auto [id, k] = release_order_.front();
     FileRecord& f = files_.at(id);
-    if (!f.finalized) break;
+    SubSeg& s = f.segs[k];
+    const bool last = s.off + s.len == f.expected;
+    if (last ? !f.finalized : !(s.accounted == s.len && hashed_through(f, s.off + s.len))) break;
     release_order_.pop_front();
     try {
-      pool_.release(f.segment_id);
+      if (!last) pool_.begin_flush(s.id);
+      pool_.release(s.id);
     } catch (const std::exception& e) {
       fail_locked(e.what());
     }
-    seg_to_file_.erase(f.segment_id);
+    s.released = true;
+    seg_to_file_.erase(s.id);
+    if (!last) continue;
     --pending_files_;
     if (f.on_done) {
       auto cb = f.on_done;

@@ -553,6 +553,7 @@ class EngineConfig:
     force_copy_engine: bool = False
     hugepages: bool = False
     flush_discard: bool = False
+    stream_segment_bytes: int = 0
 
     def _c(self) -> N.EngineConfigC:
         c = N.EngineConfigC()

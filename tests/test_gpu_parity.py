@@ -26,6 +26,9 @@ VARIANTS = {
     "kernel-only": {"force_kernel": True},
     "copy-engine-only": {"force_copy_engine": True},
     "tiny-groups": {"group_bytes": 4096, "chunk_quantum": 1500, "kernel_ctas": 3},
+    # pool far smaller than the files: every file streams through odd-sized
+    # segments with backpressure (C4 mode), bytes must not change
+    "streaming": {"stream_segment_bytes": 1_000_003, "host_buffer_bytes": 3_000_009, "chunk_quantum": 262_147},
 }
 
 
@@ -38,9 +41,10 @@ def gpu(lz):
 def run_capture(lz, w, thr, root, spec_dir, **knobs):
     spec = w.write_spec(os.path.join(spec_dir, w.name + ".spec"))
     built = lz.build_workload(spec, 0)
-    cfg = lz.EngineConfig(checkpoint_root=str(root), host_buffer_bytes=max(2 * built.bytes, 1 << 20) + (8 << 20),
-                          large_leaf_threshold=thr, fsync_on_finalize=False,
-                          **{k: v for k, v in knobs.items()})
+    knobs = dict(knobs)
+    pool = knobs.pop("host_buffer_bytes", max(2 * built.bytes, 1 << 20) + (8 << 20))
+    cfg = lz.EngineConfig(checkpoint_root=str(root), host_buffer_bytes=pool,
+                          large_leaf_threshold=thr, fsync_on_finalize=False, **knobs)
     eng = lz.Engine(cfg, built.topo, built.rank)
     t = eng.capture(lz.plan_checkpoint(built.topo, built.model, built.step), built.tree, built.step)
     eng.update_barrier(t)
@@ -400,4 +404,29 @@ def test_pool_backpressure_blocks_capture_until_flush_releases(gpu, tmp_path):
                                     large_leaf_threshold=4096)
         e2 = lz.Engine(small_cfg, topo, lz.RankCoord())
         e2.capture(lz.plan_checkpoint(topo, tiny_model(lz), 1), big, 1)
+    eng.close()
+
+
+def test_streaming_c1_through_a_small_pool(gpu, oracle, tmp_path):
+    """C1 (1.74 GB) through a 256 MB pool in 48 MB segments: golden digests,
+    capture never blocks, the fence waits for the storage tier."""
+    lz = gpu
+    from paper_2406_10707_b200.workloads import gpt2_small
+    w = gpt2_small()
+    spec = w.write_spec(str(tmp_path / "c1.spec"))
+    built = lz.build_workload(spec, 0)
+    root = tmp_path / "c1s"
+    cfg = lz.EngineConfig(checkpoint_root=str(root), host_buffer_bytes=256 << 20, stream_segment_bytes=48 << 20,
+                          fsync_on_finalize=False)
+    eng = lz.Engine(cfg, built.topo, built.rank)
+    t0 = time.perf_counter()
+    t = eng.capture(lz.plan_checkpoint(built.topo, built.model, 1), built.tree, 1)
+    assert time.perf_counter() - t0 < 1.0  # no wait for the 1.7 GB to drain
+    eng.update_barrier(t)
+    eng.wait_persisted(t)
+    got = {}
+    for f in t.shard_files():
+        data = np.fromfile(f, dtype=np.uint8)
+        got[os.path.relpath(f, root)] = (data.size, oracle.fnv64(data))
+    assert got == C1_GOLDEN
     eng.close()

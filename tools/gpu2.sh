@@ -1,4 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -30 > gpurun_out/pytest_gpu.log
-tail -3 gpurun_out/pytest_gpu.log
-timeout 900 python tools/sweep.py 1073741824 > gpurun_out/sweep.jsonl 2> gpurun_out/sweep.err; echo "sweep rc=$?"
-cat gpurun_out/sweep.jsonl; tail -3 gpurun_out/sweep.err
+timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -40 > gpurun_out/pytest_gpu.log
+tail -25 gpurun_out/pytest_gpu.log
