@@ -10,8 +10,9 @@
 //   read_entry / restore                                        :330-379
 // B200 changes: all small region leaves of a capture are snapshotted by ONE
 // gather launch into pinned staging (the reference pays one locked clone per
-// leaf); restore streams each file once into pinned staging, checks every
-// entry checksum in parallel, then DMAs leaves into fresh HBM regions.
+// leaf); restore streams each file once through pinned windows (the
+// reference reads it three times), hashing entries in parallel and DMAing
+// them into fresh HBM regions while the next window is read.
 #include "lzckpt/engine.hpp"
 
 #include <fcntl.h>
@@ -65,7 +66,7 @@ struct Pinned {
     p = nullptr;
     cap = 0;
     void* q = nullptr;
-    ck(lzk_host_alloc(std::max<uint64_t>(n, 1), LZK_HOST_MAPPED, &q), "pinned staging");
+    ck(lzk_host_alloc(std::max<uint64_t>(n, 1), LZK_HOST_MAPPED | LZK_HOST_HUGEPAGE, &q), "pinned staging");
     p = static_cast<std::byte*>(q);
     cap = n;
   }
@@ -645,54 +646,169 @@ std::vector<std::byte> read_entry(const std::filesystem::path& file, const Check
 
 namespace {
 
-// One committed shard file, read once into pinned staging and validated.
-struct LoadedFile {
-  std::filesystem::path path;
-  CheckpointFileHeader header;
-  uint64_t header_size = 0;
-  Pinned payload;  // bytes [header_size, payload_end)
-
-  const std::byte* entry_bytes(const HeaderEntry& e) const { return payload.p + (e.offset - header_size); }
+// Where one entry's bytes go during restore.
+struct EntrySink {
+  void* device = nullptr;                 // region memory (DMA target), or
+  std::vector<std::byte>* host = nullptr; // a host buffer (blobs, __meta__)
 };
 
-void load_and_validate(LoadedFile& lf) {
-  lf.header = read_header(lf.path);
-  lf.header_size = lf.header.serialized_size();
-  const uint64_t end = lf.header.payload_end();
-  const int fd = ::open(lf.path.c_str(), O_RDONLY | O_CLOEXEC);
-  if (fd < 0) throw IoError("cannot open " + lf.path.string());
-  struct Closer {
-    int fd;
-    ~Closer() { ::close(fd); }
-  } closer{fd};
-  const uint64_t size = uint64_t(::lseek(fd, 0, SEEK_END));
-  if (size != end) {
+// Streams one committed shard file through a few pinned windows: a reader
+// thread preads window i+1 while window i is hashed (FNV-1a per entry,
+// continued across windows; different entries of a window in parallel) and
+// DMA'd into its sinks. Memory stays bounded by the windows whatever the file
+// size (C2's optimizer file is 84 GB). Returns the keys whose checksum
+// mismatches (the caller decides what that voids).
+class FileStreamer {
+ public:
+  static constexpr uint64_t kWindow = 512ull << 20;
+  static constexpr int kWindows = 3;
+
+  FileStreamer(int device, uint64_t ce_threshold) : device_(device), ce_threshold_(ce_threshold) {
+    ck(lzk_stream_create(device, 0, &stream_), "restore stream");
+    for (auto& w : win_) ck(lzk_event_create(device, 1, &w.done), "restore event");
+  }
+  ~FileStreamer() {
+    for (auto& w : win_) {
+      if (w.done) lzk_event_destroy(w.done);
+      lzk_host_free(w.buf);
+    }
+    lzk_stream_destroy(stream_);
+  }
+
+  std::vector<std::string> run(const std::filesystem::path& path, const CheckpointFileHeader& h,
+                               const std::vector<EntrySink>& sinks) {
+    const uint64_t hsize = h.serialized_size(), end = h.payload_end();
+    const int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
+    if (fd < 0) throw IoError("cannot open " + path.string());
+    struct Closer {
+      int fd;
+      ~Closer() { ::close(fd); }
+    } closer{fd};
+    const uint64_t n = end - hsize;
+    const uint64_t wsize = std::min(kWindow, std::max<uint64_t>(n, 1));
+    for (auto& w : win_) {
+      if (w.cap < wsize) {
+        lzk_host_free(w.buf);
+        void* p = nullptr;
+        ck(lzk_host_alloc(wsize, LZK_HOST_MAPPED | LZK_HOST_HUGEPAGE, &p), "restore window");
+        w.buf = static_cast<std::byte*>(p);
+        w.cap = wsize;
+      }
+      w.used = false;
+    }
+    std::vector<uint64_t> state(h.entries.size(), Fnv64::kOffset);
+    const size_t nwin = size_t((n + wsize - 1) / wsize);
+    // reader: window i -> slot i % kWindows (waits until the slot's DMA finished)
+    auto read_window = [&](size_t i) {
+      Window& w = win_[i % kWindows];
+      if (w.used) ck(lzk_event_sync(w.done), "restore window reuse");
+      const uint64_t off = uint64_t(i) * wsize, len = std::min(wsize, n - off);
+      const uint64_t piece = 64ull << 20;
+      parallel_for(size_t((len + piece - 1) / piece), 8, [&](size_t k) {
+        const uint64_t o = uint64_t(k) * piece;
+        pread_all(fd, w.buf + o, std::min(piece, len - o), hsize + off + o, path);
+      });
+    };
+    std::thread reader;
+    std::exception_ptr read_err;
+    if (nwin) read_window(0);
+    for (size_t i = 0; i < nwin; ++i) {
+      if (reader.joinable()) reader.join();
+      if (read_err) std::rethrow_exception(read_err);
+      if (i + 1 < nwin) {
+        reader = std::thread([&, i] {
+          try {
+            read_window(i + 1);
+          } catch (...) {
+            read_err = std::current_exception();
+          }
+        });
+      }
+      Window& w = win_[i % kWindows];
+      const uint64_t off = uint64_t(i) * wsize, len = std::min(wsize, n - off);
+      // entry slices overlapping [off, off + len) of the payload
+      struct Slice {
+        size_t e;
+        uint64_t a, b;  // payload-relative
+      };
+      std::vector<Slice> sl;
+      for (size_t e = 0; e < h.entries.size(); ++e) {
+        const uint64_t eb = h.entries[e].offset - hsize, ee = eb + h.entries[e].length;
+        const uint64_t a = std::max(eb, off), b = std::min(ee, off + len);
+        if (a < b) sl.push_back({e, a, b});
+      }
+      std::vector<lzk_copy_desc> ce, small;
+      for (const auto& x : sl) {
+        const EntrySink& s = sinks[x.e];
+        const uint64_t eb = h.entries[x.e].offset - hsize;
+        if (s.device) {
+          lzk_copy_desc d{reinterpret_cast<uint64_t>(w.buf + (x.a - off)),
+                          reinterpret_cast<uint64_t>(static_cast<std::byte*>(s.device) + (x.a - eb)), x.b - x.a};
+          (h.entries[x.e].length >= ce_threshold_ ? ce : small).push_back(d);
+        } else if (s.host) {
+          std::memcpy(s.host->data() + (x.a - eb), w.buf + (x.a - off), x.b - x.a);
+        }
+      }
+      if (!small.empty()) ck(lzk_scatter_h2d(stream_, small.data(), uint32_t(small.size()), 0), "restore scatter");
+      if (!ce.empty()) ck(lzk_ce_copy_h2d(stream_, ce.data(), uint32_t(ce.size())), "restore DMA");
+      ck(lzk_event_record(w.done, stream_), "restore event");
+      w.used = true;
+      parallel_for(sl.size(), io_threads(), [&](size_t k) {
+        const Slice& x = sl[k];
+        state[x.e] = Fnv64::fold(state[x.e], w.buf + (x.a - off), x.b - x.a);
+      });
+    }
+    if (reader.joinable()) reader.join();
+    if (read_err) std::rethrow_exception(read_err);
+    ck(lzk_stream_sync(stream_), "restore sync");
+    std::vector<std::string> bad;
+    for (size_t e = 0; e < h.entries.size(); ++e) {
+      if (state[e] != h.entries[e].checksum) bad.push_back(h.entries[e].key);
+    }
+    return bad;
+  }
+
+ private:
+  struct Window {
+    std::byte* buf = nullptr;
+    uint64_t cap = 0;
+    lzk_event* done = nullptr;
+    bool used = false;
+  };
+  int device_;
+  uint64_t ce_threshold_;
+  lzk_stream* stream_ = nullptr;
+  Window win_[kWindows];
+};
+
+// Header + exact-extent check (reference read_header + validate_entries
+// length rule, format.cpp:173-214) and the parsed __meta__ leaf manifest.
+std::vector<LeafManifestEntry> open_shard(const std::filesystem::path& path, CheckpointFileHeader& h) {
+  h = read_header(path);
+  std::error_code ec;
+  const uint64_t size = std::filesystem::file_size(path, ec);
+  if (ec) throw IoError("cannot stat " + path.string());
+  if (size != h.payload_end()) {
     throw TruncatedFile("file length " + std::to_string(size) + " does not match declared extent " +
-                        std::to_string(end));
+                        std::to_string(h.payload_end()));
   }
-  const uint64_t n = end - lf.header_size;
-  lf.payload.ensure(n);
-  const uint64_t piece = 64ull << 20;
-  const size_t pieces = size_t((n + piece - 1) / piece);
-  parallel_for(pieces, io_threads(), [&](size_t i) {
-    const uint64_t off = uint64_t(i) * piece;
-    pread_all(fd, lf.payload.p + off, std::min(piece, n - off), lf.header_size + off, lf.path);
-  });
-  // Entry checksums in parallel, largest entries first.
-  std::vector<size_t> order(lf.header.entries.size());
-  for (size_t i = 0; i < order.size(); ++i) order[i] = i;
-  std::sort(order.begin(), order.end(),
-            [&](size_t a, size_t b) { return lf.header.entries[a].length > lf.header.entries[b].length; });
-  std::vector<char> bad(order.size(), 0);
-  parallel_for(order.size(), io_threads(), [&](size_t k) {
-    const HeaderEntry& e = lf.header.entries[order[k]];
-    bad[order[k]] = fnv64(lf.entry_bytes(e), e.length) != e.checksum;
-  });
+  auto meta = read_entry(path, h, StateTree::kMetaKey);
+  if (fnv64(meta.data(), meta.size()) != h.find(StateTree::kMetaKey)->checksum) {
+    // corrupt metadata: report every bad entry, as the reference's
+    // validate-before-parse order does (engine.cpp:360-367)
+    auto bad = validate_entries(path, h);
+    std::string keys;
+    for (const auto& k : bad) keys += (keys.empty() ? "" : ", ") + k;
+    throw ChecksumMismatch(path.string() + ": corrupt entries: " + keys);
+  }
+  return parse_leaf_manifest(meta);
+}
+
+void throw_bad(const std::filesystem::path& path, const std::vector<std::string>& bad) {
+  if (bad.empty()) return;
   std::string keys;
-  for (size_t i = 0; i < bad.size(); ++i) {
-    if (bad[i]) keys += (keys.empty() ? "" : ", ") + lf.header.entries[i].key;
-  }
-  if (!keys.empty()) throw ChecksumMismatch(lf.path.string() + ": corrupt entries: " + keys);
+  for (const auto& k : bad) keys += (keys.empty() ? "" : ", ") + k;
+  throw ChecksumMismatch(path.string() + ": corrupt entries: " + keys);
 }
 
 }  // namespace
@@ -701,67 +817,78 @@ StateTree Engine::restore(const ManifestStore& manifest, uint64_t step) const {
   const auto files = manifest.files_for(step);  // NotCommitted
   const std::string prefix = step_dirname(step) + "/" + rank_dirname(rank_) + "/";
   const int dev = transfers_.device();
-  lzk_stream* s = nullptr;
-  ck(lzk_stream_create(dev, 0, &s), "restore stream");
-  struct StreamGuard {
-    lzk_stream* s;
-    ~StreamGuard() { lzk_stream_destroy(s); }
-  } guard{s};
-
+  FileStreamer streamer(dev, config_.snapshot.ce_threshold);
   StateTree tree;
-  LoadedFile lf;
   for (const auto& rec : files) {
     if (rec.relative_path.rfind(prefix, 0) != 0) continue;
-    lf.path = config_.checkpoint_root / rec.relative_path;
-    load_and_validate(lf);
-    const HeaderEntry* me = lf.header.find(StateTree::kMetaKey);
-    if (!me) throw FormatError(lf.path.string() + ": no entry named '" + std::string(StateTree::kMetaKey) + "'");
-    std::vector<std::byte> meta(lf.entry_bytes(*me), lf.entry_bytes(*me) + me->length);
-    auto leaves = parse_leaf_manifest(meta);
-
-    std::vector<lzk_copy_desc> ce, small;
-    Pinned inline_stage;
-    uint64_t inline_total = 0;
-    for (const auto& l : leaves) {
-      if (l.inlined && l.is_region) inline_total += l.size;
-    }
-    inline_stage.ensure(inline_total);
-    uint64_t inline_off = 0;
-    for (auto& l : leaves) {
-      const std::byte* src = nullptr;
-      if (l.inlined) {
-        if (l.inline_bytes.size() != l.size) {
-          throw FormatError(lf.path.string() + ": leaf '" + l.path + "' size mismatch");
-        }
-      } else {
-        const HeaderEntry* e = lf.header.find(l.path);
-        if (!e) throw FormatError(lf.path.string() + ": no entry named '" + l.path + "'");
-        if (e->length != l.size) throw FormatError(lf.path.string() + ": leaf '" + l.path + "' size mismatch");
-        src = lf.entry_bytes(*e);
+    const std::filesystem::path path = config_.checkpoint_root / rec.relative_path;
+    CheckpointFileHeader h;
+    auto leaves = open_shard(path, h);
+    // every entry's destination: fresh regions (large region leaves), host
+    // buffers (large blobs, __meta__); inline leaves come from the manifest
+    std::vector<EntrySink> sinks(h.entries.size());
+    std::vector<std::vector<std::byte>> hostbufs(h.entries.size());
+    std::vector<std::shared_ptr<DeviceRegion>> regions(leaves.size());
+    for (size_t e = 0; e < h.entries.size(); ++e) {
+      if (h.entries[e].key == StateTree::kMetaKey) {
+        hostbufs[e].resize(h.entries[e].length);
+        sinks[e].host = &hostbufs[e];
       }
-      if (!l.is_region) {
-        if (l.inlined) {
-          tree.set_blob(l.path, std::move(l.inline_bytes));
-        } else {
-          tree.set_blob(l.path, std::vector<std::byte>(src, src + l.size));
-        }
+    }
+    for (size_t i = 0; i < leaves.size(); ++i) {
+      const auto& l = leaves[i];
+      if (l.inlined) {
+        if (l.inline_bytes.size() != l.size) throw FormatError(path.string() + ": leaf '" + l.path + "' size mismatch");
         continue;
       }
-      auto region = std::make_shared<DeviceRegion>(DeviceRegion::Uninitialized{}, l.size, dev);
-      if (l.inlined) {
-        std::memcpy(inline_stage.p + inline_off, l.inline_bytes.data(), l.size);
-        src = inline_stage.p + inline_off;
-        inline_off += l.size;
+      const HeaderEntry* he = h.find(l.path);
+      if (!he) throw FormatError(path.string() + ": no entry named '" + l.path + "'");
+      if (he->length != l.size) throw FormatError(path.string() + ": leaf '" + l.path + "' size mismatch");
+      const size_t e = size_t(he - h.entries.data());
+      if (l.is_region) {
+        regions[i] = std::make_shared<DeviceRegion>(DeviceRegion::Uninitialized{}, l.size, dev);
+        sinks[e].device = regions[i]->device_ptr();
+      } else {
+        hostbufs[e].resize(l.size);
+        sinks[e].host = &hostbufs[e];
       }
-      if (l.size) {
-        lzk_copy_desc d{reinterpret_cast<uint64_t>(src), reinterpret_cast<uint64_t>(region->device_ptr()), l.size};
-        (l.size >= config_.snapshot.ce_threshold ? ce : small).push_back(d);
-      }
-      tree.set_region(l.path, std::move(region));
     }
-    if (!small.empty()) ck(lzk_scatter_h2d(s, small.data(), uint32_t(small.size()), 0), "restore scatter");
-    if (!ce.empty()) ck(lzk_ce_copy_h2d(s, ce.data(), uint32_t(ce.size())), "restore DMA");
-    ck(lzk_stream_sync(s), "restore sync");  // staging is reused by the next file
+    throw_bad(path, streamer.run(path, h, sinks));  // reads each byte once
+    std::vector<lzk_copy_desc> inl;
+    Pinned stage;
+    uint64_t inline_total = 0;
+    for (const auto& l : leaves) inline_total += (l.inlined && l.is_region) ? l.size : 0;
+    stage.ensure(inline_total);
+    uint64_t so = 0;
+    for (size_t i = 0; i < leaves.size(); ++i) {
+      auto& l = leaves[i];
+      if (l.inlined) {
+        if (l.is_region) {
+          regions[i] = std::make_shared<DeviceRegion>(DeviceRegion::Uninitialized{}, l.size, dev);
+          if (l.size) {
+            std::memcpy(stage.p + so, l.inline_bytes.data(), l.size);
+            inl.push_back({reinterpret_cast<uint64_t>(stage.p + so), reinterpret_cast<uint64_t>(regions[i]->device_ptr()),
+                           l.size});
+            so += l.size;
+          }
+          tree.set_region(l.path, regions[i]);
+        } else {
+          tree.set_blob(l.path, std::move(l.inline_bytes));
+        }
+      } else if (l.is_region) {
+        tree.set_region(l.path, regions[i]);
+      } else {
+        tree.set_blob(l.path, std::move(hostbufs[size_t(h.find(l.path) - h.entries.data())]));
+      }
+    }
+    if (!inl.empty()) {
+      lzk_stream* s = nullptr;
+      ck(lzk_stream_create(dev, 0, &s), "restore stream");
+      int rc = lzk_scatter_h2d(s, inl.data(), uint32_t(inl.size()), 0);
+      if (rc == LZK_OK) rc = lzk_stream_sync(s);
+      lzk_stream_destroy(s);
+      ck(rc, "restore inline leaves");
+    }
   }
   return tree;
 }
@@ -770,60 +897,64 @@ void Engine::restore_into(const ManifestStore& manifest, uint64_t step, StateTre
   const auto files = manifest.files_for(step);
   const std::string prefix = step_dirname(step) + "/" + rank_dirname(rank_) + "/";
   const int dev = transfers_.device();
-  lzk_stream* s = nullptr;
-  ck(lzk_stream_create(dev, 0, &s), "restore stream");
-  struct StreamGuard {
-    lzk_stream* s;
-    ~StreamGuard() { lzk_stream_destroy(s); }
-  } guard{s};
-
-  LoadedFile lf;
+  FileStreamer streamer(dev, config_.snapshot.ce_threshold);
+  struct Plan {
+    std::filesystem::path path;
+    CheckpointFileHeader h;
+    std::vector<LeafManifestEntry> leaves;
+  };
+  std::vector<Plan> plans;
+  // pass 1: every file's structure and checksums, before any live region is touched
   for (const auto& rec : files) {
     if (rec.relative_path.rfind(prefix, 0) != 0) continue;
-    lf.path = config_.checkpoint_root / rec.relative_path;
-    load_and_validate(lf);  // nothing touches live regions before this passes
-    const HeaderEntry* me = lf.header.find(StateTree::kMetaKey);
-    if (!me) throw FormatError(lf.path.string() + ": missing " + std::string(StateTree::kMetaKey));
-    auto leaves = parse_leaf_manifest(std::vector<std::byte>(lf.entry_bytes(*me), lf.entry_bytes(*me) + me->length));
-    // Check the whole file against the tree before writing anything.
-    for (const auto& l : leaves) {
+    Plan p;
+    p.path = config_.checkpoint_root / rec.relative_path;
+    p.leaves = open_shard(p.path, p.h);
+    for (const auto& l : p.leaves) {
       if (l.is_region) {
         auto r = tree.region_at(l.path);
         if (r->size() != l.size) throw FormatError("restore_into: '" + l.path + "' size mismatch");
         if (r->device() != dev) throw ConfigError("restore_into: '" + l.path + "' on another device");
       }
-      if (!l.inlined && !lf.header.find(l.path)) {
-        throw FormatError(lf.path.string() + ": no entry named '" + l.path + "'");
-      }
+      if (!l.inlined && !p.h.find(l.path)) throw FormatError(p.path.string() + ": no entry named '" + l.path + "'");
     }
-    std::vector<lzk_copy_desc> ce, small;
-    Pinned inline_stage;
-    uint64_t inline_total = 0;
-    for (const auto& l : leaves) {
-      if (l.inlined && l.is_region) inline_total += l.size;
-    }
-    inline_stage.ensure(inline_total);
-    uint64_t inline_off = 0;
+    throw_bad(p.path, streamer.run(p.path, p.h, std::vector<EntrySink>(p.h.entries.size())));
+    plans.push_back(std::move(p));
+  }
+  // pass 2: DMA into the live regions (blobs are host state, left to restore())
+  for (auto& p : plans) {
+    std::vector<EntrySink> sinks(p.h.entries.size());
     std::vector<std::shared_ptr<DeviceRegion>> touched;
-    for (auto& l : leaves) {
-      const std::byte* src = l.inlined ? nullptr : lf.entry_bytes(*lf.header.find(l.path));
-      if (!l.is_region) continue;  // blobs are host state: handled below
+    std::vector<lzk_copy_desc> inl;
+    Pinned stage;
+    uint64_t inline_total = 0;
+    for (const auto& l : p.leaves) inline_total += (l.inlined && l.is_region) ? l.size : 0;
+    stage.ensure(inline_total);
+    uint64_t so = 0;
+    for (const auto& l : p.leaves) {
+      if (!l.is_region) continue;
       auto r = tree.region_at(l.path);
+      r->bump_version();  // an in-flight capture of this region would be torn
       if (l.inlined) {
-        std::memcpy(inline_stage.p + inline_off, l.inline_bytes.data(), l.size);
-        src = inline_stage.p + inline_off;
-        inline_off += l.size;
-      }
-      if (l.size) {
-        lzk_copy_desc d{reinterpret_cast<uint64_t>(src), reinterpret_cast<uint64_t>(r->device_ptr()), l.size};
-        (l.size >= config_.snapshot.ce_threshold ? ce : small).push_back(d);
+        if (l.size) {
+          std::memcpy(stage.p + so, l.inline_bytes.data(), l.size);
+          inl.push_back({reinterpret_cast<uint64_t>(stage.p + so), reinterpret_cast<uint64_t>(r->device_ptr()), l.size});
+          so += l.size;
+        }
+      } else {
+        sinks[size_t(p.h.find(l.path) - p.h.entries.data())].device = r->device_ptr();
       }
       touched.push_back(std::move(r));
     }
-    for (auto& r : touched) r->bump_version();  // an in-flight capture of these would be torn
-    if (!small.empty()) ck(lzk_scatter_h2d(s, small.data(), uint32_t(small.size()), 0), "restore scatter");
-    if (!ce.empty()) ck(lzk_ce_copy_h2d(s, ce.data(), uint32_t(ce.size())), "restore DMA");
-    ck(lzk_stream_sync(s), "restore sync");
+    throw_bad(p.path, streamer.run(p.path, p.h, sinks));
+    if (!inl.empty()) {
+      lzk_stream* s = nullptr;
+      ck(lzk_stream_create(dev, 0, &s), "restore stream");
+      int rc = lzk_scatter_h2d(s, inl.data(), uint32_t(inl.size()), 0);
+      if (rc == LZK_OK) rc = lzk_stream_sync(s);
+      lzk_stream_destroy(s);
+      ck(rc, "restore inline leaves");
+    }
   }
 }
 
