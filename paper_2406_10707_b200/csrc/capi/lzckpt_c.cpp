@@ -475,7 +475,7 @@ void lzckpt_engine_config_defaults(lzckpt_engine_config* c) {
   c->group_bytes = so.group_bytes;
   c->force_kernel = 0;
   c->force_copy_engine = 0;
-  c->hugepages = 0;
+  c->hugepages = 1;
   c->flush_discard = 0;
   c->stream_segment_bytes = 0;
 }

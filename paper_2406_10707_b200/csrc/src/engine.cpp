@@ -686,8 +686,10 @@ class FileStreamer {
     } closer{fd};
     const uint64_t n = end - hsize;
     const uint64_t wsize = std::min(kWindow, std::max<uint64_t>(n, 1));
-    for (auto& w : win_) {
-      if (w.cap < wsize) {
+    const size_t slots = size_t(std::min<uint64_t>(kWindows, (n + wsize - 1) / wsize));
+    for (size_t k = 0; k < size_t(kWindows); ++k) {
+      Window& w = win_[k];
+      if (k < slots && w.cap < wsize) {
         lzk_host_free(w.buf);
         void* p = nullptr;
         ck(lzk_host_alloc(wsize, LZK_HOST_MAPPED | LZK_HOST_HUGEPAGE, &p), "restore window");

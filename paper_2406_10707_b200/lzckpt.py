@@ -551,7 +551,7 @@ class EngineConfig:
     group_bytes: int = 256 << 20
     force_kernel: bool = False
     force_copy_engine: bool = False
-    hugepages: bool = False
+    hugepages: bool = True
     flush_discard: bool = False
     stream_segment_bytes: int = 0
 

@@ -4,7 +4,8 @@ liblzckpt_b200.so by tests/reftests/Makefile, with our doctest shim) on the
 GPU: transfer (D2H engine, chunk order, torn detection, pacing), flush
 (header-last, abandon, injected failure, interleaving), buffer pool
 (backpressure, timeouts), engine (round trip, inline capture, statuses,
-blocking capture), state tree, plus the host-only suites."""
+blocking capture), state tree, consolidation (2PC), verify/bench harnesses,
+plus the host-only suites."""
 import os
 import subprocess
 
@@ -12,7 +13,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SUITES = ["test_transfer", "test_flush", "test_buffer_pool", "test_engine", "test_state_tree", "test_ring",
-          "test_format", "test_topology", "test_manifest"]
+          "test_format", "test_topology", "test_manifest", "test_consolidation", "test_verify_bench"]
 
 
 @pytest.mark.gpu
@@ -24,3 +25,16 @@ def test_reference_suite_passes(suite):
     summary = r.stderr.strip().splitlines()[-1] if r.stderr.strip() else ""
     assert r.returncode == 0, r.stderr[-4000:]
     assert "| 0 failed |" in summary and summary.endswith(" 0 failed"), summary
+
+
+@pytest.mark.gpu
+def test_acceptance_criterion_1_consistency():
+    """reference acceptance criterion 1 with its seeds and bounds, driven by
+    tests/reftests/acceptance_hotpath.cpp: 500 honest round trips byte-exact
+    and committed; >= 95/100 skip-barrier trials caught torn, 0 committed;
+    under 120 s."""
+    exe = os.path.join(ROOT, "tests", "reftests", "bin", "acceptance_hotpath")
+    assert os.path.exists(exe)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr[-2000:]
+    assert "PASS" in r.stdout
