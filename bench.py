@@ -297,41 +297,30 @@ def main_ours(args, rank, world, local_rank):
         if not args.skip_streaming:
             eng.close()
             del eng
-            s_pool = 16 << 30
-            scfg = lz.EngineConfig(checkpoint_root=os.path.join(tmp, "ckpt_s"), host_buffer_bytes=s_pool,
-                                   large_leaf_threshold=1 << 20, fsync_on_finalize=False, flush_discard=True,
-                                   hugepages=True, device=dev, stream_segment_bytes=1 << 30)
-            seng = lz.Engine(scfg, built.topo, built.rank)
-            sms = []
-            for s in range(3):
-                barrier()
-                h0 = time.perf_counter()
-                t = seng.capture(plan, built.tree, 300 + s)
-                seng.update_barrier(t)
-                dt = time.perf_counter() - h0
-                seng.wait_persisted(t)
-                if s:
-                    sms.append(dt)
-            streaming = {"pool_bytes": s_pool, "segment_bytes": 1 << 30,
-                         "gbps": round(payload * len(sms) / sum(sms) / 1e9, 3),
-                         "note": "C4 mode: shard (%.1f GB) > pool; per-segment reservation with backpressure, "
-                                 "host-memory tier" % (payload / 1e9)}
-            seng.close()
-            del seng
+            try:
+                streaming = measure_streaming(lz, built, plan, payload, tmp, dev, barrier)
+                log(f"[bench] rank {rank}: streaming through a 16 GiB pool: {streaming['gbps']} GB/s")
+            except Exception as e:  # optional phase: keep the headline number
+                streaming = {"error": f"{type(e).__name__}: {e}"}
             eng = lz.Engine(cfg, built.topo, built.rank)
-            log(f"[bench] rank {rank}: streaming through a 16 GiB pool: {streaming['gbps']} GB/s")
 
         # ---- per-iteration stall under synthetic fwd/bwd (device-side fence) ----
         stall = None
         if not args.skip_train:
-            stall = train_loop(lz, torch, eng, plan, built, payload, per_gpu, barrier)
+            try:
+                stall = train_loop(lz, torch, eng, plan, built, payload, per_gpu, barrier)
+            except Exception as e:
+                stall = {"error": f"{type(e).__name__}: {e}"}
 
         # ---- e2e: public API, files durable on local disk ----
         e2e = None
         if not args.skip_e2e:
             eng.close()
             del eng
-            e2e = e2e_persisted(lz, torch, dev, tmp, args)
+            try:
+                e2e = e2e_persisted(lz, torch, dev, tmp, args, world)
+            except Exception as e:
+                e2e = {"error": f"{type(e).__name__}: {e}"}
 
         if rank == 0:
             kernel_gbps = variants["gather_kernel"]
@@ -374,6 +363,31 @@ def main_ours(args, rank, world, local_rank):
             print(json.dumps(line), flush=True)
     finally:
         shutil.rmtree(tmp, ignore_errors=True)
+
+
+def measure_streaming(lz, built, plan, payload, tmp, dev, barrier, pool=16 << 30, segment=1 << 30):
+    """C4 mode (SURVEY.md §7 hard part 3): the whole shard streams through a
+    pinned pool 1/7 its size in 1 GiB segments reserved with backpressure."""
+    scfg = lz.EngineConfig(checkpoint_root=os.path.join(tmp, "ckpt_s"), host_buffer_bytes=pool,
+                           large_leaf_threshold=1 << 20, fsync_on_finalize=False, flush_discard=True,
+                           hugepages=True, device=dev, stream_segment_bytes=segment)
+    seng = lz.Engine(scfg, built.topo, built.rank)
+    try:
+        sms = []
+        for s in range(3):
+            barrier()
+            h0 = time.perf_counter()
+            t = seng.capture(plan, built.tree, 300 + s)
+            seng.update_barrier(t)
+            dt = time.perf_counter() - h0
+            seng.wait_persisted(t)
+            if s:
+                sms.append(dt)
+    finally:
+        seng.close()
+    return {"pool_bytes": pool, "segment_bytes": segment, "gbps": round(payload * len(sms) / sum(sms) / 1e9, 3),
+            "note": "C4 mode: shard (%.1f GB) > pool; per-segment reservation with backpressure, host-memory tier"
+                    % (payload / 1e9)}
 
 
 def measure_link_ceiling(lz, dev, nbytes=8 << 30, chunk=256 << 20):
@@ -498,12 +512,14 @@ def train_loop(lz, torch, eng, plan, built, payload, gbps, barrier):
             "fence": "update_barrier_on_stream (device-side)", "gemm": "bf16 8192^3 torch.matmul x%d" % n_mm}
 
 
-def e2e_persisted(lz, torch, dev, tmp, args):
+def e2e_persisted(lz, torch, dev, tmp, args, world=1):
     """Public API end to end with durable files: capture -> update_barrier ->
     wait_persisted (pwrite + per-entry FNV + header last + fsync) on a
-    bounded C2 slice that fits local disk (1 decoder layer + embeddings)."""
+    bounded C2 slice that fits the box's local disk (all ranks write to it:
+    2 decoder layers + embeddings at N<=2, 1 layer at N>2)."""
     from paper_2406_10707_b200.workloads import llama7b_shard
-    w = llama7b_shard(layers=2, vocab=8000, name="c2-slice-2l")
+    layers = 2 if world <= 2 else 1
+    w = llama7b_shard(layers=layers, vocab=8000, name=f"c2-slice-{layers}l")
     spec = w.write_spec(os.path.join(tmp, "e2e.spec"))
     built = lz.build_workload(spec, dev)
     root = os.path.join(tmp, "e2e_ckpt")

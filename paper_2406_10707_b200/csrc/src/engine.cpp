@@ -21,6 +21,8 @@
 #include <algorithm>
 #include <atomic>
 #include <cerrno>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <utility>
@@ -39,6 +41,22 @@ void ck(int rc, const char* what) {
 double since(std::chrono::steady_clock::time_point t0) {
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
+
+// LZCKPT_TRACE=1: per-phase capture timing on stderr (host-overhead tuning).
+struct PhaseTrace {
+  bool on = std::getenv("LZCKPT_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  std::string line;
+  void mark(const char* name) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    line += std::string(" ") + name + "=" + std::to_string(std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+  ~PhaseTrace() {
+    if (on) std::fprintf(stderr, "[lzckpt capture ms]%s\n", line.c_str());
+  }
+};
 
 struct ShardBuild {
   const ShardDescriptor* shard = nullptr;
@@ -225,6 +243,7 @@ void Engine::snapshot_inline_leaves(InlineSnapshot& snap) const {
 std::shared_ptr<CaptureTicket> Engine::capture(const CheckpointPlan& plan, const StateTree& state,
                                                uint64_t step) {
   const auto t0 = std::chrono::steady_clock::now();
+  PhaseTrace tr;
   const auto& shards = plan.shards(flat_rank(topo_, rank_));
   const auto names = state.top_level_names();
   if (names.size() != shards.size()) {
@@ -272,7 +291,9 @@ std::shared_ptr<CaptureTicket> Engine::capture(const CheckpointPlan& plan, const
       inline_buf_ = static_cast<std::byte*>(p);
       inline_cap_ = snap.bytes;
     }
+    tr.mark("flatten+validate");
     snapshot_inline_leaves(snap);
+    tr.mark("inline_gather");
 
     size_t next_inline = 0;
     for (size_t i = 0; i < shards.size(); ++i) {
@@ -313,6 +334,7 @@ std::shared_ptr<CaptureTicket> Engine::capture(const CheckpointPlan& plan, const
     }
   }
 
+  tr.mark("meta+header");
   auto ticket = std::shared_ptr<CaptureTicket>(new CaptureTicket());
   {
     std::lock_guard lk(mu_);
@@ -435,7 +457,9 @@ std::shared_ptr<CaptureTicket> Engine::capture(const CheckpointPlan& plan, const
       dst += b.larges[k].size;
       tasks.push_back(std::move(t));
     }
+    tr.mark("reserve+register+tasks");
     transfers_.submit_copies(ticket->id_, std::move(tasks));
+    tr.mark("submit");
     total += b.payload;
   }
   ticket->payload_bytes_ = total;
