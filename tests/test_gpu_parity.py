@@ -430,3 +430,112 @@ def test_streaming_c1_through_a_small_pool(gpu, oracle, tmp_path):
         got[os.path.relpath(f, root)] = (data.size, oracle.fnv64(data))
     assert got == C1_GOLDEN
     eng.close()
+
+
+@pytest.mark.parametrize("variant", ["kernel", "copy_engine"])
+def test_tensor_larger_than_4gib_misaligned(gpu, tmp_path, variant):
+    """A 4.5 GiB + 7 B leaf after a 13 B meta-sized offset: 64-bit sizes and
+    offsets through the gather kernel and the DMA path, checked by sampled
+    windows (head, 4 GiB boundary, tail) against the device bytes."""
+    lz = gpu
+    torch = pytest.importorskip("torch")
+    n = (9 << 29) + 7
+    big = torch.empty(n, dtype=torch.uint8, device="cuda")
+    d = lz.dev
+    import ctypes as C
+    s = C.c_void_p()
+    assert d.lzk_stream_create(0, 0, C.byref(s)) == 0
+    assert d.lzk_fill_splitmix(s, big.data_ptr(), n, 99, 3) == 0
+    assert d.lzk_stream_sync(s) == 0
+    d.lzk_stream_destroy(s)
+    topo = lz.ParallelTopology(1, 1, 1, 1, 1)
+    params = (n + 13) // 2  # layer shard = 2 B/param; optimizer gets the rest
+    model = lz.ModelSpec(param_count=params, layer_count=1)
+    plan = lz.plan_checkpoint(topo, model, 1)
+    layer_bytes, opt_bytes = [x.size_bytes for x in plan.shards(0)]
+    tree = lz.StateTree()
+    tree.set_region("a/big", lz.DeviceRegion.wrap(big))
+    tree.set_blob("a/pad", bytes(layer_bytes - n))
+    opt = torch.zeros(opt_bytes, dtype=torch.uint8, device="cuda")
+    tree.set_region("b/o", lz.DeviceRegion.wrap(opt))
+    cfg = lz.EngineConfig(checkpoint_root=str(tmp_path), host_buffer_bytes=layer_bytes + opt_bytes + (64 << 20),
+                          fsync_on_finalize=False, large_leaf_threshold=1 << 20,
+                          force_kernel=variant == "kernel", force_copy_engine=variant == "copy_engine")
+    eng = lz.Engine(cfg, topo, lz.RankCoord())
+    t = eng.capture(plan, tree, 1)
+    eng.update_barrier(t)
+    eng.wait_persisted(t)
+    f = [p for p in t.shard_files() if "layers" in p][0]
+    h = lz.read_header(f)
+    e = h.find("a/big")
+    assert e.length == n
+    with open(f, "rb") as fh:
+        for off in (0, (1 << 32) - 4096, n - 5000):
+            fh.seek(e.offset + off)
+            got = fh.read(5000)
+            assert got == big[off:off + 5000].cpu().numpy().tobytes(), off
+    assert lz.validate_entries(f, h) == []
+    eng.close()
+
+
+def test_unpaced_mutation_before_barrier_is_torn(gpu, tmp_path):
+    """Fast path (device-issued copies): a declared mutation that lands while
+    the D2H is still running tears the ticket; no file gets a header."""
+    lz = gpu
+    torch = pytest.importorskip("torch")
+    topo = lz.ParallelTopology(1, 1, 1, 1, 1)
+    n = 2 << 30
+    model = lz.ModelSpec(param_count=n // 2, layer_count=1)
+    plan = lz.plan_checkpoint(topo, model, 1)
+    lb, ob = [x.size_bytes for x in plan.shards(0)]
+    w = torch.zeros(lb, dtype=torch.uint8, device="cuda")
+    o = torch.zeros(ob, dtype=torch.uint8, device="cuda")
+    tree = lz.StateTree()
+    rw = lz.DeviceRegion.wrap(w)
+    tree.set_region("a/w", rw)
+    tree.set_region("b/o", lz.DeviceRegion.wrap(o))
+    cfg = lz.EngineConfig(checkpoint_root=str(tmp_path), host_buffer_bytes=lb + ob + (64 << 20),
+                          fsync_on_finalize=False)
+    eng = lz.Engine(cfg, topo, lz.RankCoord())
+    t = eng.capture(plan, tree, 1)
+    rw.write(0, b"\x01")  # ~0.3 s of D2H still ahead (14 GB)
+    with pytest.raises(lz.TornSnapshot):
+        eng.update_barrier(t)
+    with pytest.raises(lz.TornSnapshot):
+        eng.wait_persisted(t)
+    eng.drain()
+    for f in t.shard_files():
+        with pytest.raises(lz.BadMagic):
+            lz.read_header(f)
+    eng.close()
+
+
+def test_rejected_captures_reserve_nothing(gpu, tmp_path):
+    """reference test_engine.cpp:141-170: a plan/tree mismatch or the reserved
+    metadata name throws before any pool space is taken."""
+    lz = gpu
+    eng, topo = small_engine(lz, tmp_path)
+    plan = lz.plan_checkpoint(topo, tiny_model(lz), 1)
+    one = lz.StateTree()
+    one.set_region("layers/w", lz.DeviceRegion(8192))
+    with pytest.raises(lz.ConfigError):  # one child, two shards
+        eng.capture(plan, one, 1)
+    wrong = lz.StateTree()
+    wrong.set_region("layers/w", lz.DeviceRegion(8000))
+    wrong.set_region("optim/m", lz.DeviceRegion(49152))
+    with pytest.raises(lz.ConfigError):  # sizes do not match the plan
+        eng.capture(plan, wrong, 1)
+    meta = lz.StateTree()
+    meta.set_region("__meta__", lz.DeviceRegion(8192))
+    meta.set_region("optim/m", lz.DeviceRegion(49152))
+    with pytest.raises(lz.DuplicatePath):
+        eng.capture(plan, meta, 1)
+    assert eng.counters().captures == 0
+    ok = lz.StateTree()
+    ok.set_region("layers/w", lz.DeviceRegion(8192))
+    ok.set_region("optim/m", lz.DeviceRegion(49152))
+    t = eng.capture(plan, ok, 1)  # the pool is still whole
+    eng.update_barrier(t)
+    eng.wait_persisted(t)
+    assert t.status() == "persisted"
+    eng.close()

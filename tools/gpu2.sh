@@ -1,3 +1,1 @@
-timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -20 > gpurun_out/pytest_gpu.log
-tail -6 gpurun_out/pytest_gpu.log
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 1500 python -m pytest tests/test_gpu_parity.py -m gpu -q -k "4gib or unpaced_mutation_before or rejected" 2>&1 | tail -25
