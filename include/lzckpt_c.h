@@ -234,6 +234,13 @@ typedef struct lzckpt_snapshot_stats {
 int lzckpt_engine_snapshot_stats(const lzckpt_engine* e, lzckpt_snapshot_stats* out);
 /* bytes the flush pipeline has written, files it persisted */
 int lzckpt_engine_flush_stats(const lzckpt_engine* e, uint64_t* bytes_written, uint64_t* files_persisted);
+/* Framework glue (DeepSpeed-style checkpoint engine): one LZCKPT01 file for
+ * every leaf of the tree, same lazy snapshot path, no plan. */
+int lzckpt_engine_capture_file(lzckpt_engine* e, const char* path, const lzckpt_tree* t, uint64_t step,
+                               lzckpt_ticket** out);
+/* Reads one file back (validated). Region leaves are DMA'd into the
+ * same-path, same-size regions of `into` (may be NULL), else fresh regions. */
+int lzckpt_engine_restore_file(lzckpt_engine* e, const char* path, const lzckpt_tree* into, lzckpt_tree** out);
 /* Switches the D2H variant for later captures (B200 tuning knob). */
 int lzckpt_engine_set_copy_variant(lzckpt_engine* e, uint64_t ce_threshold, int force_kernel, int force_copy_engine,
                                    uint32_t kernel_ctas, uint64_t group_bytes);

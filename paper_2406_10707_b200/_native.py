@@ -141,6 +141,8 @@ ENGINE_SYMBOLS = [
     ("lzckpt_engine_flush_stats", i32, [vp, P(u64), P(u64)]),
     ("lzckpt_engine_snapshot_stream", vp, [vp]),
     ("lzckpt_engine_set_copy_variant", i32, [vp, u64, i32, i32, u32, u64]),
+    ("lzckpt_engine_capture_file", i32, [vp, cp, vp, u64, P(vp)]),
+    ("lzckpt_engine_restore_file", i32, [vp, cp, vp, P(vp)]),
     ("lzckpt_ticket_release", None, [vp]),
     ("lzckpt_ticket_id", u64, [vp]),
     ("lzckpt_ticket_step", u64, [vp]),

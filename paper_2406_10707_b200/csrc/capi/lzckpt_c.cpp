@@ -600,6 +600,28 @@ int lzckpt_engine_flush_stats(const lzckpt_engine* e, uint64_t* bytes_written, u
   });
 }
 
+int lzckpt_engine_capture_file(lzckpt_engine* e, const char* path, const lzckpt_tree* t, uint64_t step,
+                               lzckpt_ticket** out) {
+  return guard([&] {
+    need(e, "engine");
+    need(path, "path");
+    need(t, "tree");
+    need(out, "out");
+    *out = new lzckpt_ticket{e->e->capture_file(path, t->t, step)};
+  });
+}
+
+int lzckpt_engine_restore_file(lzckpt_engine* e, const char* path, const lzckpt_tree* into, lzckpt_tree** out) {
+  return guard([&] {
+    need(e, "engine");
+    need(path, "path");
+    need(out, "out");
+    auto t = std::make_unique<lzckpt_tree>();
+    t->t = e->e->restore_file(path, into ? &into->t : nullptr);
+    *out = t.release();
+  });
+}
+
 int lzckpt_engine_set_copy_variant(lzckpt_engine* e, uint64_t ce_threshold, int force_kernel, int force_copy_engine,
                                    uint32_t kernel_ctas, uint64_t group_bytes) {
   return guard([&] {

@@ -59,7 +59,7 @@ struct PhaseTrace {
 };
 
 struct ShardBuild {
-  const ShardDescriptor* shard = nullptr;
+  uint64_t shard_id = 0;
   std::filesystem::path path;
   CheckpointFileHeader header;
   std::vector<LeafManifestEntry> manifest;
@@ -243,7 +243,6 @@ void Engine::snapshot_inline_leaves(InlineSnapshot& snap) const {
 std::shared_ptr<CaptureTicket> Engine::capture(const CheckpointPlan& plan, const StateTree& state,
                                                uint64_t step) {
   const auto t0 = std::chrono::steady_clock::now();
-  PhaseTrace tr;
   const auto& shards = plan.shards(flat_rank(topo_, rank_));
   const auto names = state.top_level_names();
   if (names.size() != shards.size()) {
@@ -251,21 +250,43 @@ std::shared_ptr<CaptureTicket> Engine::capture(const CheckpointPlan& plan, const
                       " top-level children but the plan assigns " + std::to_string(shards.size()) +
                       " shards to this rank");
   }
-
   // Validate everything before the first reservation (a rejected capture
   // must not strand a segment).
-  std::vector<ShardBuild> builds(shards.size());
-  std::vector<std::vector<StateTree::FlatLeaf>> leaves(shards.size());
-  InlineSnapshot snap;
+  std::vector<FileSpec> files(shards.size());
   for (size_t i = 0; i < shards.size(); ++i) {
-    leaves[i] = state.flatten_child(names[i]);
+    files[i].path = shard_path(config_.checkpoint_root, step, shards[i]);
+    files[i].shard_id = shards[i].shard_id;
+    files[i].leaves = state.flatten_child(names[i]);
     uint64_t sum = 0;
-    for (const auto& l : leaves[i]) sum += l.size;
+    for (const auto& l : files[i].leaves) sum += l.size;
     if (sum != shards[i].size_bytes) {
       throw ConfigError("subtree '" + names[i] + "' holds " + std::to_string(sum) + " bytes but shard " +
                         shards[i].filename() + " expects " + std::to_string(shards[i].size_bytes));
     }
-    for (const auto& l : leaves[i]) {
+  }
+  return capture_impl(files, step, t0);
+}
+
+std::shared_ptr<CaptureTicket> Engine::capture_file(const std::filesystem::path& path, const StateTree& state,
+                                                    uint64_t step) {
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<FileSpec> files(1);
+  files[0].path = path;
+  files[0].leaves = state.flatten();
+  uint64_t sum = 0;
+  for (const auto& l : files[0].leaves) sum += l.size;
+  if (files[0].leaves.empty()) throw ConfigError("capture_file: empty state tree");
+  (void)sum;
+  return capture_impl(files, step, t0);
+}
+
+std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files, uint64_t step,
+                                                    std::chrono::steady_clock::time_point t0) {
+  PhaseTrace tr;
+  std::vector<ShardBuild> builds(files.size());
+  InlineSnapshot snap;
+  for (auto& f : files) {
+    for (const auto& l : f.leaves) {
       if (l.path == StateTree::kMetaKey) {
         throw DuplicatePath("top-level leaf name '" + l.path + "' is reserved");
       }
@@ -296,12 +317,13 @@ std::shared_ptr<CaptureTicket> Engine::capture(const CheckpointPlan& plan, const
     tr.mark("inline_gather");
 
     size_t next_inline = 0;
-    for (size_t i = 0; i < shards.size(); ++i) {
+    for (size_t i = 0; i < files.size(); ++i) {
       ShardBuild& b = builds[i];
-      b.shard = &shards[i];
-      b.path = shard_path(config_.checkpoint_root, step, shards[i]);
-      b.manifest.reserve(leaves[i].size());
-      for (auto& l : leaves[i]) {
+      b.shard_id = files[i].shard_id;
+      b.path = files[i].path;
+      const auto& leaves_i = files[i].leaves;
+      b.manifest.reserve(leaves_i.size());
+      for (auto& l : leaves_i) {
         LeafManifestEntry e;
         e.path = l.path;
         e.is_region = l.region != nullptr;
@@ -322,7 +344,7 @@ std::shared_ptr<CaptureTicket> Engine::capture(const CheckpointPlan& plan, const
       b.meta = std::make_shared<const std::vector<std::byte>>(serialize_leaf_manifest(b.manifest));
       b.manifest.clear();
       b.header.entries.push_back({std::string(StateTree::kMetaKey), 0, b.meta->size(), 0});
-      for (const auto& l : leaves[i]) {
+      for (const auto& l : leaves_i) {
         if (l.size >= config_.large_leaf_threshold) b.header.entries.push_back({l.path, 0, l.size, 0});
       }
       uint64_t cursor = b.header.serialized_size();
@@ -385,7 +407,7 @@ std::shared_ptr<CaptureTicket> Engine::capture(const CheckpointPlan& plan, const
           if (n) {
             auto t = std::make_shared<CopyTask>();
             t->ticket = ticket->id_;
-            t->shard_id = b.shard->shard_id;
+            t->shard_id = b.shard_id;
             t->source.region = src.region;
             t->source.host_blob = src.region ? nullptr : src.blob;
             t->src_offset = soff;
@@ -437,7 +459,7 @@ std::shared_ptr<CaptureTicket> Engine::capture(const CheckpointPlan& plan, const
     tasks.reserve(1 + b.larges.size());
     auto meta = std::make_shared<CopyTask>();
     meta->ticket = ticket->id_;
-    meta->shard_id = b.shard->shard_id;
+    meta->shard_id = b.shard_id;
     meta->source.host_blob = b.meta;
     meta->length = b.meta->size();
     meta->segment_id = seg.id;
@@ -447,7 +469,7 @@ std::shared_ptr<CaptureTicket> Engine::capture(const CheckpointPlan& plan, const
     for (size_t k = 0; k < b.larges.size(); ++k) {
       auto t = std::make_shared<CopyTask>();
       t->ticket = ticket->id_;
-      t->shard_id = b.shard->shard_id;
+      t->shard_id = b.shard_id;
       t->source.region = b.larges[k].region;
       t->source.host_blob = b.larges[k].blob;
       t->length = b.larges[k].size;
@@ -839,83 +861,112 @@ void throw_bad(const std::filesystem::path& path, const std::vector<std::string>
 
 }  // namespace
 
+namespace {
+
+// One validated shard file into `tree`: region leaves DMA'd into the
+// same-path, same-size regions of `into` when present, else fresh regions;
+// blobs and inline leaves from host bytes. Reads each byte once.
+void restore_one(const std::filesystem::path& path, StateTree& tree, const StateTree* into, int dev,
+                 FileStreamer& streamer) {
+  CheckpointFileHeader h;
+  auto leaves = open_shard(path, h);
+  std::vector<EntrySink> sinks(h.entries.size());
+  std::vector<std::vector<std::byte>> hostbufs(h.entries.size());
+  std::vector<std::shared_ptr<DeviceRegion>> regions(leaves.size());
+  auto region_for = [&](const LeafManifestEntry& l) {
+    if (into && into->has(l.path)) {
+      try {
+        auto r = into->region_at(l.path);
+        if (r->size() == l.size && r->device() == dev) {
+          r->bump_version();  // contents are being replaced
+          return r;
+        }
+      } catch (const Error&) {
+        // a blob at that path: fall through to a fresh region
+      }
+    }
+    return std::make_shared<DeviceRegion>(DeviceRegion::Uninitialized{}, l.size, dev);
+  };
+  for (size_t e = 0; e < h.entries.size(); ++e) {
+    if (h.entries[e].key == StateTree::kMetaKey) {
+      hostbufs[e].resize(h.entries[e].length);
+      sinks[e].host = &hostbufs[e];
+    }
+  }
+  for (size_t i = 0; i < leaves.size(); ++i) {
+    const auto& l = leaves[i];
+    if (l.inlined) {
+      if (l.inline_bytes.size() != l.size) throw FormatError(path.string() + ": leaf '" + l.path + "' size mismatch");
+      continue;
+    }
+    const HeaderEntry* he = h.find(l.path);
+    if (!he) throw FormatError(path.string() + ": no entry named '" + l.path + "'");
+    if (he->length != l.size) throw FormatError(path.string() + ": leaf '" + l.path + "' size mismatch");
+    const size_t e = size_t(he - h.entries.data());
+    if (l.is_region) {
+      regions[i] = region_for(l);
+      sinks[e].device = regions[i]->device_ptr();
+    } else {
+      hostbufs[e].resize(l.size);
+      sinks[e].host = &hostbufs[e];
+    }
+  }
+  throw_bad(path, streamer.run(path, h, sinks));
+  std::vector<lzk_copy_desc> inl;
+  Pinned stage;
+  uint64_t inline_total = 0;
+  for (const auto& l : leaves) inline_total += (l.inlined && l.is_region) ? l.size : 0;
+  stage.ensure(inline_total);
+  uint64_t so = 0;
+  for (size_t i = 0; i < leaves.size(); ++i) {
+    auto& l = leaves[i];
+    if (l.inlined) {
+      if (l.is_region) {
+        regions[i] = region_for(l);
+        if (l.size) {
+          std::memcpy(stage.p + so, l.inline_bytes.data(), l.size);
+          inl.push_back({reinterpret_cast<uint64_t>(stage.p + so), reinterpret_cast<uint64_t>(regions[i]->device_ptr()),
+                         l.size});
+          so += l.size;
+        }
+        tree.set_region(l.path, regions[i]);
+      } else {
+        tree.set_blob(l.path, std::move(l.inline_bytes));
+      }
+    } else if (l.is_region) {
+      tree.set_region(l.path, regions[i]);
+    } else {
+      tree.set_blob(l.path, std::move(hostbufs[size_t(h.find(l.path) - h.entries.data())]));
+    }
+  }
+  if (!inl.empty()) {
+    lzk_stream* s = nullptr;
+    ck(lzk_stream_create(dev, 0, &s), "restore stream");
+    int rc = lzk_scatter_h2d(s, inl.data(), uint32_t(inl.size()), 0);
+    if (rc == LZK_OK) rc = lzk_stream_sync(s);
+    lzk_stream_destroy(s);
+    ck(rc, "restore inline leaves");
+  }
+}
+
+}  // namespace
+
 StateTree Engine::restore(const ManifestStore& manifest, uint64_t step) const {
   const auto files = manifest.files_for(step);  // NotCommitted
   const std::string prefix = step_dirname(step) + "/" + rank_dirname(rank_) + "/";
-  const int dev = transfers_.device();
-  FileStreamer streamer(dev, config_.snapshot.ce_threshold);
+  FileStreamer streamer(transfers_.device(), config_.snapshot.ce_threshold);
   StateTree tree;
   for (const auto& rec : files) {
     if (rec.relative_path.rfind(prefix, 0) != 0) continue;
-    const std::filesystem::path path = config_.checkpoint_root / rec.relative_path;
-    CheckpointFileHeader h;
-    auto leaves = open_shard(path, h);
-    // every entry's destination: fresh regions (large region leaves), host
-    // buffers (large blobs, __meta__); inline leaves come from the manifest
-    std::vector<EntrySink> sinks(h.entries.size());
-    std::vector<std::vector<std::byte>> hostbufs(h.entries.size());
-    std::vector<std::shared_ptr<DeviceRegion>> regions(leaves.size());
-    for (size_t e = 0; e < h.entries.size(); ++e) {
-      if (h.entries[e].key == StateTree::kMetaKey) {
-        hostbufs[e].resize(h.entries[e].length);
-        sinks[e].host = &hostbufs[e];
-      }
-    }
-    for (size_t i = 0; i < leaves.size(); ++i) {
-      const auto& l = leaves[i];
-      if (l.inlined) {
-        if (l.inline_bytes.size() != l.size) throw FormatError(path.string() + ": leaf '" + l.path + "' size mismatch");
-        continue;
-      }
-      const HeaderEntry* he = h.find(l.path);
-      if (!he) throw FormatError(path.string() + ": no entry named '" + l.path + "'");
-      if (he->length != l.size) throw FormatError(path.string() + ": leaf '" + l.path + "' size mismatch");
-      const size_t e = size_t(he - h.entries.data());
-      if (l.is_region) {
-        regions[i] = std::make_shared<DeviceRegion>(DeviceRegion::Uninitialized{}, l.size, dev);
-        sinks[e].device = regions[i]->device_ptr();
-      } else {
-        hostbufs[e].resize(l.size);
-        sinks[e].host = &hostbufs[e];
-      }
-    }
-    throw_bad(path, streamer.run(path, h, sinks));  // reads each byte once
-    std::vector<lzk_copy_desc> inl;
-    Pinned stage;
-    uint64_t inline_total = 0;
-    for (const auto& l : leaves) inline_total += (l.inlined && l.is_region) ? l.size : 0;
-    stage.ensure(inline_total);
-    uint64_t so = 0;
-    for (size_t i = 0; i < leaves.size(); ++i) {
-      auto& l = leaves[i];
-      if (l.inlined) {
-        if (l.is_region) {
-          regions[i] = std::make_shared<DeviceRegion>(DeviceRegion::Uninitialized{}, l.size, dev);
-          if (l.size) {
-            std::memcpy(stage.p + so, l.inline_bytes.data(), l.size);
-            inl.push_back({reinterpret_cast<uint64_t>(stage.p + so), reinterpret_cast<uint64_t>(regions[i]->device_ptr()),
-                           l.size});
-            so += l.size;
-          }
-          tree.set_region(l.path, regions[i]);
-        } else {
-          tree.set_blob(l.path, std::move(l.inline_bytes));
-        }
-      } else if (l.is_region) {
-        tree.set_region(l.path, regions[i]);
-      } else {
-        tree.set_blob(l.path, std::move(hostbufs[size_t(h.find(l.path) - h.entries.data())]));
-      }
-    }
-    if (!inl.empty()) {
-      lzk_stream* s = nullptr;
-      ck(lzk_stream_create(dev, 0, &s), "restore stream");
-      int rc = lzk_scatter_h2d(s, inl.data(), uint32_t(inl.size()), 0);
-      if (rc == LZK_OK) rc = lzk_stream_sync(s);
-      lzk_stream_destroy(s);
-      ck(rc, "restore inline leaves");
-    }
+    restore_one(config_.checkpoint_root / rec.relative_path, tree, nullptr, transfers_.device(), streamer);
   }
+  return tree;
+}
+
+StateTree Engine::restore_file(const std::filesystem::path& path, const StateTree* into) const {
+  FileStreamer streamer(transfers_.device(), config_.snapshot.ce_threshold);
+  StateTree tree;
+  restore_one(path, tree, into, transfers_.device(), streamer);
   return tree;
 }
 

@@ -645,6 +645,17 @@ class Engine:
         _check(lib.lzckpt_engine_capture(self._h, C.byref(plan.model._c()), state._h, step, C.byref(h)))
         return CaptureTicket(h)
 
+    def capture_file(self, path, state: StateTree, step: int) -> CaptureTicket:
+        h = C.c_void_p()
+        _check(lib.lzckpt_engine_capture_file(self._h, os.fspath(path).encode(), state._h, step, C.byref(h)))
+        return CaptureTicket(h)
+
+    def restore_file(self, path, into: Optional[StateTree] = None) -> StateTree:
+        h = C.c_void_p()
+        _check(lib.lzckpt_engine_restore_file(self._h, os.fspath(path).encode(), into._h if into else None,
+                                              C.byref(h)))
+        return StateTree(_handle=h)
+
     def update_barrier(self, t: CaptureTicket) -> None:
         _check(lib.lzckpt_engine_update_barrier(self._h, t._h))
 

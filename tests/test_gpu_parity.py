@@ -539,3 +539,55 @@ def test_rejected_captures_reserve_nothing(gpu, tmp_path):
     eng.wait_persisted(t)
     assert t.status() == "persisted"
     eng.close()
+
+
+def test_deepspeed_style_checkpoint_engine_roundtrip(gpu, tmp_path):
+    """Framework glue: a torch model + Adam state saved through the
+    DeepSpeed-style engine while training continues after wait(); load()
+    returns exactly the snapshot taken at save time (all dtypes, CPU tensors,
+    non-contiguous views, scalars, nested containers)."""
+    torch = pytest.importorskip("torch")
+    from paper_2406_10707_b200.checkpoint_engine import DataStatesCheckpointEngine
+    torch.manual_seed(0)
+    model = torch.nn.Sequential(torch.nn.Linear(512, 1024), torch.nn.GELU(), torch.nn.Linear(1024, 256)).cuda()
+    model[2].to(torch.bfloat16)
+    opt = torch.optim.Adam(model.parameters(), lr=1e-3)
+    for _ in range(2):
+        x = torch.randn(64, 512, device="cuda")
+        out = model[2](model[1](model[0](x)).to(torch.bfloat16))
+        out.float().pow(2).mean().backward()
+        opt.step()
+        opt.zero_grad()
+    extra = {"step": 7, "lr": [1e-3, 2e-4], "cpu_buf": torch.arange(10, dtype=torch.int64),
+             "view": torch.randn(32, 64, device="cuda").t(), "empty": torch.empty(0, device="cuda"),
+             "scalar": torch.tensor(3.5, device="cuda"), ("tuple", "key"): None}
+    state = {"module": model.state_dict(), "optimizer": opt.state_dict(), "extra": extra}
+    expect = {k: v.detach().clone().cpu() for k, v in model.state_dict().items()}
+    expect_opt = {k: {n: (t.detach().clone().cpu() if torch.is_tensor(t) else t) for n, t in st.items()}
+                  for k, st in opt.state_dict()["state"].items()}
+    eng = DataStatesCheckpointEngine({"datastates_ckpt": {"host_cache_size": 64 << 20, "fsync": False}})
+    eng.create("global_step7")
+    eng.makedirs(str(tmp_path / "global_step7"), exist_ok=True)
+    eng.save(state, str(tmp_path / "global_step7" / "mp_rank_00_model_states.pt"))
+    eng.wait(torch.cuda.current_stream())  # device-side lazy fence
+    x = torch.randn(64, 512, device="cuda")  # training continues: mutates params and Adam state
+    model[2](model[1](model[0](x)).to(torch.bfloat16)).float().sum().backward()
+    opt.step()
+    assert eng.commit("global_step7")
+    back = eng.load(str(tmp_path / "global_step7" / "mp_rank_00_model_states.pt"))
+    for k, v in expect.items():
+        got = back["module"][k]
+        assert got.dtype == v.dtype and got.is_cuda and torch.equal(got.cpu(), v), k
+    for k, st in expect_opt.items():
+        for n, t in st.items():
+            g = back["optimizer"]["state"][k][n]
+            assert torch.equal(g.cpu(), t) if torch.is_tensor(t) else g == t
+    assert back["optimizer"]["param_groups"] == opt.state_dict()["param_groups"]
+    e = back["extra"]
+    assert e["step"] == 7 and e["lr"] == [1e-3, 2e-4] and e[("tuple", "key")] is None
+    assert torch.equal(e["cpu_buf"], extra["cpu_buf"]) and not e["cpu_buf"].is_cuda
+    assert torch.equal(e["view"].cpu(), extra["view"].cpu()) and e["view"].shape == (64, 32)
+    assert e["empty"].numel() == 0 and float(e["scalar"]) == 3.5
+    cpu = eng.load(str(tmp_path / "global_step7" / "mp_rank_00_model_states.pt"), map_location="cpu")
+    assert all(not t.is_cuda for t in cpu["module"].values())
+    eng.close()
