@@ -591,3 +591,31 @@ def test_deepspeed_style_checkpoint_engine_roundtrip(gpu, tmp_path):
     cpu = eng.load(str(tmp_path / "global_step7" / "mp_rank_00_model_states.pt"), map_location="cpu")
     assert all(not t.is_cuda for t in cpu["module"].values())
     eng.close()
+
+
+def test_restores_files_written_by_the_reference_engine(gpu, oracle, cases, tmp_path):
+    """Cross-implementation: the reference engine (oracle/_ref/ref_snapshot,
+    built from the reference sources) writes and commits a checkpoint; our
+    engine restores it from the reference's own manifest, byte-exact."""
+    import json
+    import subprocess
+    lz = gpu
+    drv = os.path.join(ROOT, "oracle", "_ref", "ref_snapshot")
+    assert os.path.exists(drv), "oracle/_ref not built (run __graft_entry__.build() where /root/reference exists)"
+    w, thr = cases["odd-sizes"]
+    spec = w.write_spec(str(tmp_path / "w.spec"))
+    root = tmp_path / "refckpt"
+    r = subprocess.run([drv, "--spec", spec, "--root", str(root), "--threshold", str(thr), "--restore", "1"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert json.loads(r.stdout)["ranks"][0]["restore_exact"]
+    topo = lz.ParallelTopology(*w.topology)
+    cfg = lz.EngineConfig(checkpoint_root=str(root), host_buffer_bytes=64 << 20, large_leaf_threshold=thr)
+    eng = lz.Engine(cfg, topo, lz.RankCoord(*w.rank))
+    m = lz.ManifestStore(root / "manifest-0.json")
+    back = eng.restore(m, w.step)
+    src = oracle.generate(w)
+    for i, (kind, path, _) in enumerate(w.leaves):
+        got = back.region_at(path).clone_bytes() if kind == "r" else back.blob_at(path)
+        assert got == src[i].tobytes(), path
+    eng.close()
