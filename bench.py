@@ -588,7 +588,7 @@ def main():
         reference_arm(args, rank, world)
         return
     if world > 1:
-        os.environ.setdefault("NCCL_DEBUG", "WARN")  # stdout carries exactly one JSON line
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout carries only our JSON
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
