@@ -42,6 +42,10 @@ struct FlushConfig {
   // a segment is released as soon as all of its bytes are resident. For
   // measuring the D2H snapshot stage on shards larger than local storage.
   bool discard = false;
+  // Verification tier: every entry is hashed exactly as for a real file, the
+  // header is built, but nothing is written (full-size parity checks on
+  // shards larger than local storage).
+  bool hash_only = false;
 };
 
 enum class FlushFileState { Pending, Persisted, Abandoned, Discarded };
@@ -74,6 +78,8 @@ class FlushPipeline {
   FlushFileState file_state(uint64_t file_id) const;
 
   uint64_t bytes_written() const;
+  // The file's header as finalized (entry checksums filled in).
+  CheckpointFileHeader file_header(uint64_t file_id) const;
   uint64_t files_persisted() const;
   size_t queue_depth() const;
 

@@ -195,6 +195,7 @@ typedef struct lzckpt_engine_config {
   int hugepages;
   int flush_discard;          /* host-memory tier only (no files) */
   uint64_t stream_segment_bytes; /* > 0: files stream through the pool in segments this large */
+  int flush_hash_only;        /* verification tier: hash every entry, write nothing */
 } lzckpt_engine_config;
 void lzckpt_engine_config_defaults(lzckpt_engine_config* c);
 
@@ -241,6 +242,8 @@ int lzckpt_engine_capture_file(lzckpt_engine* e, const char* path, const lzckpt_
 /* Reads one file back (validated). Region leaves are DMA'd into the
  * same-path, same-size regions of `into` (may be NULL), else fresh regions. */
 int lzckpt_engine_restore_file(lzckpt_engine* e, const char* path, const lzckpt_tree* into, lzckpt_tree** out);
+/* Finalized header of the ticket's i-th file (checksums as written / hashed). */
+int lzckpt_engine_ticket_header(const lzckpt_engine* e, const lzckpt_ticket* k, uint32_t i, lzckpt_header** out);
 /* Switches the D2H variant for later captures (B200 tuning knob). */
 int lzckpt_engine_set_copy_variant(lzckpt_engine* e, uint64_t ce_threshold, int force_kernel, int force_copy_engine,
                                    uint32_t kernel_ctas, uint64_t group_bytes);

@@ -92,6 +92,20 @@ void lzo_fill_splitmix(uint64_t seed, uint64_t leaf, uint64_t size, uint8_t* out
   }
 }
 
+uint64_t lzo_splitmix_fnv(uint64_t seed, uint64_t leaf, uint64_t size) {
+  const uint64_t base = seed ^ (leaf * 0xD1B54A32D192ED03ull);
+  uint64_t h = 0xcbf29ce484222325ull, k = 0, w = 0;
+  for (; k + 8 <= size; k += 8, ++w) {
+    const uint64_t v = mix64(base + (w + 1) * 0x9E3779B97F4A7C15ull);
+    for (int b = 0; b < 8; ++b) h = (h ^ ((v >> (8 * b)) & 0xff)) * 0x100000001b3ull;
+  }
+  if (k < size) {
+    const uint64_t v = mix64(base + (w + 1) * 0x9E3779B97F4A7C15ull);
+    for (uint64_t b = 0; b < size - k; ++b) h = (h ^ ((v >> (8 * b)) & 0xff)) * 0x100000001b3ull;
+  }
+  return h;
+}
+
 /* ---- ring: src/ring_core.cpp:21-139 -------------------------------------- */
 typedef struct {
   uint64_t id, off, len;

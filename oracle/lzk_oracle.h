@@ -22,6 +22,9 @@ uint64_t lzo_fnv1a64(uint64_t state, const uint8_t* p, uint64_t n);
 /* Generators (workloads.py) */
 void lzo_fill_mt19937_64(uint64_t seed, uint64_t n_leaves, const uint64_t* sizes, uint8_t* const* out);
 void lzo_fill_splitmix(uint64_t seed, uint64_t leaf, uint64_t size, uint8_t* out);
+/* FNV-1a 64 of the splitmix64 stream of (seed, leaf, size), without storing
+ * it (full-size checksum parity of GB-scale shards). */
+uint64_t lzo_splitmix_fnv(uint64_t seed, uint64_t leaf, uint64_t size);
 
 /* Ring placement state machine — src/ring_core.cpp:21-139 */
 typedef struct lzo_ring lzo_ring;

@@ -36,6 +36,8 @@ def _load():
     lib.lzo_fnv1a64.argtypes = [u64, u8p, u64]
     lib.lzo_fill_mt19937_64.argtypes = [u64, u64, C.POINTER(u64), C.POINTER(C.c_void_p)]
     lib.lzo_fill_splitmix.argtypes = [u64, u64, u64, u8p]
+    lib.lzo_splitmix_fnv.restype = u64
+    lib.lzo_splitmix_fnv.argtypes = [u64, u64, u64]
     lib.lzo_ring_new.restype = C.c_void_p
     lib.lzo_ring_new.argtypes = [u64]
     lib.lzo_ring_free.argtypes = [C.c_void_p]
@@ -180,3 +182,51 @@ def header_bytes(entries: List[Tuple[str, int, int, int]]) -> bytes:
                            (C.c_uint64 * n)(*[e[2] for e in entries]), (C.c_uint64 * n)(*[e[3] for e in entries]),
                            buf.ctypes.data)
     return buf.tobytes()
+
+
+def expected_headers(workload, threshold: int, threads: int = 16):
+    """Headers (key, offset, length, checksum) of every shard file of a
+    splitmix64 workload, computed WITHOUT materializing the payload: large
+    leaves hash their generated stream in C (threads release the GIL), the
+    __meta__ entry is composed from the (small) inline leaves. For GB-scale
+    full-size parity: compare with the engine's finalized headers."""
+    import struct
+    from concurrent.futures import ThreadPoolExecutor
+    assert workload.gen == "splitmix64"
+    dp, pp, tp, gpn, nodes = workload.topology
+    rdp, rpp, rtp = workload.rank
+    flat = (rdp * pp + rpp) * tp + rtp
+    shards = plan_rank(dp, pp, tp, workload.param_count, workload.layer_count, workload.bpp_model,
+                       workload.bpp_opt, flat)
+    tops = sorted({p.split("/")[0] for _, p, _ in workload.leaves}, key=lambda s: s.encode())
+    big = [(i, s) for i, (_, _, s) in enumerate(workload.leaves) if s >= threshold]
+    big.sort(key=lambda x: -x[1])
+    with ThreadPoolExecutor(threads) as ex:
+        digests = dict(zip([i for i, _ in big],
+                           ex.map(lambda x: L.lzo_splitmix_fnv(workload.seed, x[0], x[1]), big)))
+    out = {}
+    for top, sh in zip(tops, shards):
+        idx = [i for i, (_, p, _) in enumerate(workload.leaves) if p.split("/")[0] == top]
+        order = [idx[j] for j in flatten_order([workload.leaves[i][1] for i in idx])]
+        meta = [struct.pack("<I", len(order))]
+        large = []
+        for i in order:
+            kind, path, size = workload.leaves[i]
+            pb = path.encode()
+            inl = size < threshold
+            meta.append(struct.pack("<I", len(pb)) + pb + struct.pack("<BQ", (1 if kind == "r" else 0) | (2 if inl else 0), size))
+            if inl:
+                b = np.empty(max(size, 1), dtype=np.uint8)
+                L.lzo_fill_splitmix(workload.seed, i, size, b.ctypes.data)
+                meta.append(b[:size].tobytes())
+            else:
+                large.append((path, size, digests[i]))
+        mb = b"".join(meta)
+        entries = [("__meta__", len(mb), fnv64(mb))] + large
+        cur = 24 + sum(28 + len(k.encode()) for k, _, _ in entries)
+        hdr = []
+        for k, n, d in entries:
+            hdr.append((k, cur, n, d))
+            cur += n
+        out[f"step-{workload.step}/rank-{rdp}-{rpp}-{rtp}/{sh['filename']}"] = hdr
+    return out

@@ -52,7 +52,7 @@ class EngineConfigC(C.Structure):
                 ("flush_threads", u32), ("large_leaf_threshold", u64), ("reserve_timeout_ms", i64),
                 ("device", i32), ("ce_threshold", u64), ("kernel_ctas", u32), ("group_bytes", u64),
                 ("force_kernel", i32), ("force_copy_engine", i32), ("hugepages", i32),
-                ("flush_discard", i32), ("stream_segment_bytes", u64)]
+                ("flush_discard", i32), ("stream_segment_bytes", u64), ("flush_hash_only", i32)]
 
 
 class CountersC(C.Structure):
@@ -142,6 +142,7 @@ ENGINE_SYMBOLS = [
     ("lzckpt_engine_snapshot_stream", vp, [vp]),
     ("lzckpt_engine_set_copy_variant", i32, [vp, u64, i32, i32, u32, u64]),
     ("lzckpt_engine_capture_file", i32, [vp, cp, vp, u64, P(vp)]),
+    ("lzckpt_engine_ticket_header", i32, [vp, vp, u32, P(vp)]),
     ("lzckpt_engine_restore_file", i32, [vp, cp, vp, P(vp)]),
     ("lzckpt_ticket_release", None, [vp]),
     ("lzckpt_ticket_id", u64, [vp]),

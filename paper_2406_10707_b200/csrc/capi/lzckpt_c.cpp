@@ -478,6 +478,7 @@ void lzckpt_engine_config_defaults(lzckpt_engine_config* c) {
   c->hugepages = 1;
   c->flush_discard = 0;
   c->stream_segment_bytes = 0;
+  c->flush_hash_only = 0;
 }
 
 int lzckpt_engine_create(const lzckpt_engine_config* c, const lzckpt_topology* topo, uint32_t rank_dp,
@@ -504,6 +505,7 @@ int lzckpt_engine_create(const lzckpt_engine_config* c, const lzckpt_topology* t
     cfg.pool.hugepages = c->hugepages != 0;
     cfg.flush.discard = c->flush_discard != 0;
     cfg.stream_segment_bytes = c->stream_segment_bytes;
+    cfg.flush.hash_only = c->flush_hash_only != 0;
     auto h = std::make_unique<lzckpt_engine>();
     h->topo = to_topo(topo);
     h->e = std::make_unique<Engine>(std::move(cfg), h->topo, RankCoord{rank_dp, rank_pp, rank_tp});
@@ -619,6 +621,16 @@ int lzckpt_engine_restore_file(lzckpt_engine* e, const char* path, const lzckpt_
     auto t = std::make_unique<lzckpt_tree>();
     t->t = e->e->restore_file(path, into ? &into->t : nullptr);
     *out = t.release();
+  });
+}
+
+int lzckpt_engine_ticket_header(const lzckpt_engine* e, const lzckpt_ticket* k, uint32_t i, lzckpt_header** out) {
+  return guard([&] {
+    need(e, "engine");
+    need(k, "ticket");
+    need(out, "out");
+    auto hs = e->e->ticket_headers(k->k);
+    *out = new lzckpt_header{hs.at(i)};
   });
 }
 

@@ -664,6 +664,17 @@ TicketStatus Engine::ticket_status(const CaptureTicket& t) const {
   return TicketStatus::HostResident;
 }
 
+std::vector<CheckpointFileHeader> Engine::ticket_headers(const std::shared_ptr<CaptureTicket>& ticket) const {
+  std::vector<uint64_t> ids;
+  {
+    std::lock_guard tl(ticket->mu_);
+    for (const auto& f : ticket->files_) ids.push_back(f.flush_file_id);
+  }
+  std::vector<CheckpointFileHeader> out;
+  for (uint64_t id : ids) out.push_back(const_cast<FlushPipeline&>(flush_).file_header(id));
+  return out;
+}
+
 Engine::Counters Engine::counters() const {
   std::lock_guard lk(mu_);
   return counters_;

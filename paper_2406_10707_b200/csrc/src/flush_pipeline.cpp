@@ -77,7 +77,7 @@ uint64_t FlushPipeline::register_common(std::filesystem::path path, CheckpointFi
   f.header_size = header_size;
   f.expected = header.payload_end() - header_size;
   if (f.expected == 0) throw Error("flush file with empty payload: " + path.string());
-  if (!config_.discard) {
+  if (!config_.discard && !config_.hash_only) {
     std::error_code ec;
     std::filesystem::create_directories(path.parent_path(), ec);
     f.fd = ::open(path.c_str(), O_CREAT | O_WRONLY | O_TRUNC | O_CLOEXEC, 0644);
@@ -341,7 +341,15 @@ void FlushPipeline::worker_loop() {
   }
 }
 
+CheckpointFileHeader FlushPipeline::file_header(uint64_t file_id) const {
+  std::lock_guard lk(mu_);
+  auto it = files_.find(file_id);
+  if (it == files_.end()) throw Error("file_header: unknown flush file");
+  return it->second.header;
+}
+
 void FlushPipeline::run_write(FileRecord& f, const Job& j, const std::byte* src) {
+  if (config_.hash_only) return;  // verification tier: hashed, never written
   if (config_.storage_bandwidth_Bps > 0) {
     std::chrono::steady_clock::time_point until;
     {
@@ -470,7 +478,7 @@ void FlushPipeline::maybe_finalize(std::unique_lock<std::mutex>& lk, uint64_t id
   if (err.empty()) {
     try {
       pool_.begin_flush(last_seg);  // Filled -> Flushing
-      if (healthy && !config_.discard) {
+      if (healthy && !config_.discard && !config_.hash_only) {
         pwrite_all(f.fd, header.data(), header.size(), 0, f.path);  // header last
         if (config_.fsync_on_finalize) ::fsync(f.fd);
       }

@@ -554,6 +554,7 @@ class EngineConfig:
     hugepages: bool = True
     flush_discard: bool = False
     stream_segment_bytes: int = 0
+    flush_hash_only: bool = False
 
     def _c(self) -> N.EngineConfigC:
         c = N.EngineConfigC()
@@ -644,6 +645,14 @@ class Engine:
         h = C.c_void_p()
         _check(lib.lzckpt_engine_capture(self._h, C.byref(plan.model._c()), state._h, step, C.byref(h)))
         return CaptureTicket(h)
+
+    def ticket_headers(self, t: CaptureTicket) -> List[CheckpointFileHeader]:
+        out = []
+        for i in range(lib.lzckpt_ticket_file_count(t._h)):
+            hh = C.c_void_p()
+            _check(lib.lzckpt_engine_ticket_header(self._h, t._h, i, C.byref(hh)))
+            out.append(_from_handle(hh))
+        return out
 
     def capture_file(self, path, state: StateTree, step: int) -> CaptureTicket:
         h = C.c_void_p()

@@ -1,1 +1,1 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -k "reference_engine" 2>&1 | tail -30
+timeout 1200 python -m pytest tests/test_gpu_fullsize.py -m gpu -q -s 2>&1 | tail -8
