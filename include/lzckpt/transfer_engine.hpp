@@ -99,7 +99,7 @@ struct ThrottledChannel {
 struct SnapshotOptions {
   int device = -1;                    // -1: current device at construction
   uint64_t ce_threshold = 2ull << 20; // tasks >= this go to the copy engines
-  uint32_t kernel_ctas = 16;          // gather kernel grid (PCIe-saturating)
+  uint32_t kernel_ctas = 8;           // gather kernel grid: 4 saturate PCIe for every size class
   uint64_t group_bytes = 256ull << 20; // bytes per completion event (and max DMA size)
   int stream_priority = 1;            // > 0: below default (compute) priority
   bool force_kernel = false;          // every region chunk through the gather kernel

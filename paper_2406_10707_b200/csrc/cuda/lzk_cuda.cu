@@ -10,18 +10,21 @@
 //  * Descriptors travel as a __grid_constant__ kernel parameter (<= 32 KB),
 //    so the call needs no staging buffer and the caller's array is free the
 //    moment the launch returns. Larger batches become several launches.
-//  * Work unit = a "tile" of <= kTile bytes of one descriptor. Tile
-//    boundaries sit at 128-byte-aligned DESTINATION addresses, so only a
-//    descriptor's first tile has an unaligned head and only its last a tail.
+//  * Work unit = a warp tile: <= kTile (16 KB) bytes of one descriptor owned
+//    by one warp (16 per CTA), so many small tensors are copied in parallel
+//    by a small grid. Tile boundaries sit at 128-byte-aligned DESTINATION
+//    addresses: only a descriptor's first tile has an unaligned head and only
+//    its last a tail.
 //  * Loads: aligned 128-bit LDG of the source; when source and destination
 //    disagree mod 16, each output word is funnel-shifted out of two adjacent
 //    aligned source words (the neighbour's word hits L1).
 //  * Stores: aligned 128-bit STG; a warp writes 512 contiguous bytes that
 //    start on a 128-byte line = four full-line posted PCIe writes (ncu showed
 //    16-byte-aligned warp stores straddling five lines cost ~15% of the link).
-//  * Grid: a handful of CTAs saturates PCIe Gen5 x16 (measured on the box:
-//    >= 4 CTAs x 256 threads reach the 52.8 GB/s SM-store plateau), so the
-//    snapshot steals ~5% of the 148 SMs from training kernels.
+//  * Grid: a handful of CTAs saturates PCIe Gen5 x16 (measured: 2 CTAs for
+//    >= 1 MiB tensors; warp tiles keep 4-KiB tensors link-bound with a small
+//    grid too), so the snapshot steals only a few of the 148 SMs from
+//    training kernels.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -89,9 +92,10 @@ cudaStream_t helper_stream(int device) {
 // gather kernel
 // ---------------------------------------------------------------------------
 
-constexpr uint32_t kTile = 64u << 10;      // bytes of one descriptor per tile
-constexpr int kThreads = 512;              // 16 warps
-constexpr int kUnroll = 4;                 // 16-byte words in flight per thread per pass
+constexpr uint32_t kTile = 16u << 10;      // bytes of one descriptor per WARP work unit
+constexpr int kThreads = 512;              // 16 warps per CTA
+constexpr int kWarps = kThreads / 32;
+constexpr int kUnroll = 4;                 // 16-byte words in flight per lane per pass
 constexpr uint32_t kMaxDescPerLaunch = 960;
 
 struct Desc {
@@ -143,16 +147,16 @@ __device__ __forceinline__ uint4 extract(const uint4& a, const uint4& b, uint32_
   return o;
 }
 
-// Aligned-destination body: nw 16-byte words to dw from source words sa
-// (aligned base) at byte skew k in [1, 15].
+// Aligned-destination body, one warp: nw 16-byte words to dw from aligned
+// source words sa at byte skew k in [1, 15]. Lane l owns words l, l+32, ...
 template <int Q>
 __device__ __forceinline__ void body_skewed(const uint4* __restrict__ sa, uint4* dw, uint32_t nw,
-                                            uint32_t shift) {
-  for (uint32_t base = threadIdx.x; base < nw; base += kThreads * kUnroll) {
+                                            uint32_t shift, uint32_t lane) {
+  for (uint32_t base = lane; base < nw; base += 32 * kUnroll) {
     uint4 lo[kUnroll], hi[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      uint32_t j = base + u * kThreads;
+      const uint32_t j = base + u * 32;
       if (j < nw) {
         lo[u] = ld_cached(sa + j);
         hi[u] = ld_cached(sa + j + 1);
@@ -160,81 +164,74 @@ __device__ __forceinline__ void body_skewed(const uint4* __restrict__ sa, uint4*
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      uint32_t j = base + u * kThreads;
+      const uint32_t j = base + u * 32;
       if (j < nw) st_word(dw + j, extract<Q>(lo[u], hi[u], shift));
     }
   }
 }
 
-__device__ __forceinline__ void body_aligned(const uint4* __restrict__ sw, uint4* dw, uint32_t nw) {
-  for (uint32_t base = threadIdx.x; base < nw; base += kThreads * kUnroll) {
+__device__ __forceinline__ void body_aligned(const uint4* __restrict__ sw, uint4* dw, uint32_t nw, uint32_t lane) {
+  for (uint32_t base = lane; base < nw; base += 32 * kUnroll) {
     uint4 v[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      uint32_t j = base + u * kThreads;
+      const uint32_t j = base + u * 32;
       if (j < nw) v[u] = ld_stream(sw + j);
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      uint32_t j = base + u * kThreads;
+      const uint32_t j = base + u * 32;
       if (j < nw) st_word(dw + j, v[u]);
     }
   }
 }
 
-// Aligned-destination words [w0, w1) (word j at d + 16 j), either skewed or
-// aligned source, dispatched once per span.
-__device__ __forceinline__ void copy_words(const uint8_t* s, uint4* dw, uint32_t nw) {
+__device__ __forceinline__ void copy_words(const uint8_t* s, uint4* dw, uint32_t nw, uint32_t lane) {
   const uint32_t k = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(s) & 15u);
   if (k == 0) {
-    body_aligned(reinterpret_cast<const uint4*>(s), dw, nw);
+    body_aligned(reinterpret_cast<const uint4*>(s), dw, nw, lane);
     return;
   }
   const uint4* sa = reinterpret_cast<const uint4*>(s - k);
   const uint32_t shift = 8u * (k & 3u);
   switch (k >> 2) {
-    case 0: body_skewed<0>(sa, dw, nw, shift); break;
-    case 1: body_skewed<1>(sa, dw, nw, shift); break;
-    case 2: body_skewed<2>(sa, dw, nw, shift); break;
-    default: body_skewed<3>(sa, dw, nw, shift); break;
+    case 0: body_skewed<0>(sa, dw, nw, shift, lane); break;
+    case 1: body_skewed<1>(sa, dw, nw, shift, lane); break;
+    case 2: body_skewed<2>(sa, dw, nw, shift, lane); break;
+    default: body_skewed<3>(sa, dw, nw, shift, lane); break;
   }
 }
 
-// Copies n bytes src -> dst. Stores are shaped for the host link: bytes up to
-// the first 16-byte boundary go bytewise, then up to seven 16-byte words up
-// to the first 128-byte line boundary, then the body, where every warp
-// stores 512 bytes starting on a line boundary (four full-line posted
-// writes, never five partial ones), then the tail.
-__device__ __forceinline__ void copy_span(const uint8_t* src, uint8_t* dst, uint64_t n) {
+// One warp copies n bytes src -> dst. Stores are shaped for the host link:
+// bytes up to the first 16-byte boundary go bytewise, then up to seven
+// 16-byte words up to the first 128-byte line boundary, then the body, where
+// every warp store covers 512 bytes starting on a line boundary (four
+// full-line posted writes, never five partial ones), then the tail.
+__device__ __forceinline__ void copy_span(const uint8_t* src, uint8_t* dst, uint64_t n, uint32_t lane) {
   uint32_t head = static_cast<uint32_t>((16u - (reinterpret_cast<uintptr_t>(dst) & 15u)) & 15u);
   if (head > n) head = static_cast<uint32_t>(n);
-  if (threadIdx.x < head) dst[threadIdx.x] = src[threadIdx.x];
+  if (lane < head) dst[lane] = src[lane];
   const uint8_t* s = src + head;
   uint8_t* d = dst + head;
   uint64_t rem = n - head;
-  // 16-byte words before the first 128-byte line boundary
   uint32_t lead = static_cast<uint32_t>(((128u - (reinterpret_cast<uintptr_t>(d) & 127u)) & 127u) >> 4);
   if (lead > (rem >> 4)) lead = static_cast<uint32_t>(rem >> 4);
   if (lead) {
-    // one word per thread (threads < lead), same skew handling
-    if (threadIdx.x < 32) {
-      const uint32_t k = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(s) & 15u);
-      if (threadIdx.x < lead) {
-        const uint8_t* sw = s + 16u * threadIdx.x;
-        uint4 v;
-        if (k == 0) {
-          v = ld_cached(reinterpret_cast<const uint4*>(sw));
-        } else {
-          uint32_t b[4];
+    if (lane < lead) {
+      const uint8_t* sw = s + 16u * lane;
+      uint4 v;
+      if ((reinterpret_cast<uintptr_t>(sw) & 15u) == 0) {
+        v = ld_cached(reinterpret_cast<const uint4*>(sw));
+      } else {
+        uint32_t b[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            b[q] = uint32_t(sw[4 * q]) | (uint32_t(sw[4 * q + 1]) << 8) | (uint32_t(sw[4 * q + 2]) << 16) |
-                   (uint32_t(sw[4 * q + 3]) << 24);
-          }
-          v = make_uint4(b[0], b[1], b[2], b[3]);
+        for (int q = 0; q < 4; ++q) {
+          b[q] = uint32_t(sw[4 * q]) | (uint32_t(sw[4 * q + 1]) << 8) | (uint32_t(sw[4 * q + 2]) << 16) |
+                 (uint32_t(sw[4 * q + 3]) << 24);
         }
-        st_word(reinterpret_cast<uint4*>(d) + threadIdx.x, v);
+        v = make_uint4(b[0], b[1], b[2], b[3]);
       }
+      st_word(reinterpret_cast<uint4*>(d) + lane, v);
     }
     s += 16u * lead;
     d += 16u * lead;
@@ -242,38 +239,43 @@ __device__ __forceinline__ void copy_span(const uint8_t* src, uint8_t* dst, uint
   }
   const uint32_t nw = static_cast<uint32_t>(rem >> 4);
   const uint32_t tail = static_cast<uint32_t>(rem & 15u);
-  if (nw) copy_words(s, reinterpret_cast<uint4*>(d), nw);
-  if (threadIdx.x < tail) {
-    const uint64_t o = static_cast<uint64_t>(nw) * 16u + threadIdx.x;
+  if (nw) copy_words(s, reinterpret_cast<uint4*>(d), nw, lane);
+  if (lane < tail) {
+    const uint64_t o = static_cast<uint64_t>(nw) * 16u + lane;
     d[o] = s[o];
   }
 }
 
+// Grid-stride over warp tiles: tile t of descriptor i covers destination
+// bytes [local*kTile - mis, (local+1)*kTile - mis) clipped to the
+// descriptor, mis = dst & 127, so interior boundaries sit on 128-byte lines.
+// Each warp finds its descriptor by a warp-uniform binary search over the
+// tile prefix (broadcast constant-bank reads).
 __global__ void __launch_bounds__(kThreads)
     lzk_gather_kernel(const __grid_constant__ DescBatch batch) {
-  for (uint64_t t = blockIdx.x; t < batch.total_tiles; t += gridDim.x) {
-    // uniform binary search: last descriptor with tile_begin <= t
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t warp = uint64_t(blockIdx.x) * kWarps + (threadIdx.x >> 5);
+  const uint64_t nwarps = uint64_t(gridDim.x) * kWarps;
+  for (uint64_t t = warp; t < batch.total_tiles; t += nwarps) {
     uint32_t lo = 0, hi = batch.n - 1;
     while (lo < hi) {
-      uint32_t mid = (lo + hi + 1) >> 1;
+      const uint32_t mid = (lo + hi + 1) >> 1;
       if (batch.d[mid].tile_begin <= t) lo = mid; else hi = mid - 1;
     }
     const Desc& dsc = batch.d[lo];
     const uint64_t mis = dsc.dst & 127u;
     const uint64_t local = t - dsc.tile_begin;
-    // tile boundaries at 128-byte-aligned destination addresses: [local*kTile - mis, ...)
     const uint64_t b = local == 0 ? 0 : local * kTile - mis;
     uint64_t e = (local + 1) * kTile - mis;
     if (e > dsc.len) e = dsc.len;
-    copy_span(reinterpret_cast<const uint8_t*>(dsc.src) + b, reinterpret_cast<uint8_t*>(dsc.dst) + b,
-              e - b);
+    copy_span(reinterpret_cast<const uint8_t*>(dsc.src) + b, reinterpret_cast<uint8_t*>(dsc.dst) + b, e - b, lane);
   }
 }
 
 int launch_gather(cudaStream_t stream, const lzk_copy_desc* d, uint32_t n, uint32_t max_ctas) {
   if (n == 0) return LZK_OK;
   if (d == nullptr) return fail(LZK_ERR_INVALID, "gather: null descriptor array");
-  if (max_ctas == 0) max_ctas = 16;
+  if (max_ctas == 0) max_ctas = 8;
   // Stack-allocating 31 KB is fine for host threads; keep it static per thread.
   thread_local DescBatch batch;
   uint32_t i = 0;
@@ -291,7 +293,7 @@ int launch_gather(cudaStream_t stream, const lzk_copy_desc* d, uint32_t n, uint3
     }
     if (batch.n == 0) continue;
     batch.total_tiles = tiles;
-    uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(tiles, max_ctas));
+    uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>((tiles + kWarps - 1) / kWarps, max_ctas));
     lzk_gather_kernel<<<grid, kThreads, 0, stream>>>(batch);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "lzk_gather_kernel launch");

@@ -547,7 +547,7 @@ class EngineConfig:
     reserve_timeout_ms: int = 60_000
     device: int = -1
     ce_threshold: int = 2 << 20
-    kernel_ctas: int = 16
+    kernel_ctas: int = 8
     group_bytes: int = 256 << 20
     force_kernel: bool = False
     force_copy_engine: bool = False
