@@ -28,6 +28,11 @@
  *   lzk_host_alloc
  *       HostBufferPool's std::vector storage (src/buffer_pool.cpp:10):
  *       pinned + mapped so the copy engine and SM stores reach it directly.
+ *   lzk_fnv1a64_batch
+ *       Fnv64 / fnv64 (include/lzckpt/checksum.hpp:12-43) as used for the
+ *       per-entry checksums of FlushPipeline::write_chunk/finalize
+ *       (src/flush_pipeline.cpp:194-263) and the restore check in
+ *       validate_entries/read_entry (src/format.cpp:173-214).
  *   lzk_dev_alloc / lzk_memcpy_* / lzk_dev_memset
  *       DeviceRegion's host std::vector (include/lzckpt/transfer_engine.hpp:24-43).
  */
@@ -56,6 +61,18 @@ typedef struct lzk_copy_desc {
   uint64_t dst;
   uint64_t len;
 } lzk_copy_desc;
+
+/* One checksum: FNV-1a-64 of `len` bytes at device address `src` (any
+ * alignment), continuing from state `seed` (LZK_FNV_BASIS for a fresh
+ * digest). The 8-byte result is stored at `out`: device memory or pinned,
+ * mapped host memory. */
+typedef struct lzk_hash_desc {
+  uint64_t src;
+  uint64_t len;
+  uint64_t seed;
+  uint64_t out;
+} lzk_hash_desc;
+#define LZK_FNV_BASIS 0xcbf29ce484222325ull
 
 typedef struct lzk_stream lzk_stream;
 typedef struct lzk_event lzk_event;
@@ -124,6 +141,17 @@ int lzk_scatter_h2d(lzk_stream* s, const lzk_copy_desc* d, uint32_t n, uint32_t 
 int lzk_ce_copy_h2d(lzk_stream* s, const lzk_copy_desc* d, uint32_t n);
 /* Device-to-device multi-tensor gather (same kernel, device destination). */
 int lzk_gather_d2d(lzk_stream* s, const lzk_copy_desc* d, uint32_t n, uint32_t max_ctas);
+
+/* ---- checksums ----------------------------------------------------------- */
+/* Device FNV-1a-64 of n byte ranges in stream order, bit-identical to the
+ * reference's byte-serial fold. A bit-sliced scan of the low-byte trajectory
+ * lets the 32 lanes of a warp hash one range in parallel; ranges larger than
+ * a fair share of the grid are split into segments hashed by many warps
+ * (multi-pass). max_ctas bounds the CTAs (SMs) used; 0 = two per SM. */
+int lzk_fnv1a64_batch(lzk_stream* s, const lzk_hash_desc* d, uint32_t n, uint32_t max_ctas);
+/* Same, continuing running digests: each range's initial state is read from
+ * its `out` address (seed ignored) and the new state written back there. */
+int lzk_fnv1a64_continue(lzk_stream* s, const lzk_hash_desc* d, uint32_t n, uint32_t max_ctas);
 
 /* ---- synthetic workload generation (bench/tests) ------------------------ */
 /* Fills `bytes` of device memory with the splitmix64 counter stream of

@@ -8,6 +8,6 @@ reference ``lzckpt`` API over that C ABI.
 from .lzckpt import *  # noqa: F401,F403
 from .lzckpt import (CaptureTicket, CheckpointFileHeader, CheckpointPlan, DeviceRegion, Engine,  # noqa: F401
                      EngineConfig, HeaderEntry, ManifestStore, ModelSpec, ParallelTopology, RankCoord,
-                     RingCore, StateTree, committed_record, device_count, fnv64, kernel_launches,
+                     RingCore, StateTree, committed_record, device_count, device_fnv64, fnv64, kernel_launches,
                      parse_header, plan_checkpoint, read_entry, read_header, serialize_header,
                      validate_entries)

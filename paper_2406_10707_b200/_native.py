@@ -69,6 +69,10 @@ class CopyDescC(C.Structure):
     _fields_ = [("src", u64), ("dst", u64), ("len", u64)]
 
 
+class HashDescC(C.Structure):
+    _fields_ = [("src", u64), ("len", u64), ("seed", u64), ("out", u64)]
+
+
 P = C.POINTER
 
 # (name, restype, argtypes) of every exported C-ABI symbol; tests check that
@@ -192,6 +196,8 @@ DEVICE_SYMBOLS = [
     ("lzk_scatter_h2d", i32, [vp, P(CopyDescC), u32, u32]),
     ("lzk_ce_copy_h2d", i32, [vp, P(CopyDescC), u32]),
     ("lzk_gather_d2d", i32, [vp, P(CopyDescC), u32, u32]),
+    ("lzk_fnv1a64_batch", i32, [vp, P(HashDescC), u32, u32]),
+    ("lzk_fnv1a64_continue", i32, [vp, P(HashDescC), u32, u32]),
     ("lzk_fill_splitmix", i32, [vp, vp, u64, u64, u64]),
     ("lzk_busy_compute", i32, [vp, vp, u64, u32, u32]),
 ]

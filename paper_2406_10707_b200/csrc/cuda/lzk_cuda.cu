@@ -41,12 +41,12 @@
 
 #include <sys/mman.h>
 
-#include "lzk_cuda.h"
+#include "lzk_internal.h"
 
-namespace {
+namespace lzk_detail {
 
 thread_local std::string g_err;
-std::atomic<uint64_t> g_launches{0};
+std::atomic<uint64_t> launches{0};
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -64,18 +64,20 @@ int cuda_fail(cudaError_t e, const char* what) {
   return fail(LZK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-#define LZK_CK(call)                                   \
-  do {                                                 \
-    cudaError_t e_ = (call);                           \
-    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
-  } while (0)
-
 int use_device(int device) {
   int cur = -1;
   LZK_CK(cudaGetDevice(&cur));
   if (cur != device) LZK_CK(cudaSetDevice(device));
   return LZK_OK;
 }
+
+}  // namespace lzk_detail
+
+namespace {
+
+using lzk_detail::cuda_fail;
+using lzk_detail::fail;
+using lzk_detail::use_device;
 
 // Per-thread, per-device non-blocking stream for the synchronous helpers.
 cudaStream_t helper_stream(int device) {
@@ -297,7 +299,7 @@ int launch_gather(cudaStream_t stream, const lzk_copy_desc* d, uint32_t n, uint3
     lzk_gather_kernel<<<grid, kThreads, 0, stream>>>(batch);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "lzk_gather_kernel launch");
-    g_launches.fetch_add(1, std::memory_order_relaxed);
+    lzk_detail::launches.fetch_add(1, std::memory_order_relaxed);
   }
   return LZK_OK;
 }
@@ -347,12 +349,6 @@ __global__ void lzk_busy_kernel(float* buf, uint64_t n, uint32_t iters) {
 
 }  // namespace
 
-struct lzk_stream {
-  cudaStream_t s = nullptr;
-  int device = 0;
-  bool owned = true;
-};
-
 struct lzk_event {
   cudaEvent_t e = nullptr;
   int device = 0;
@@ -360,7 +356,7 @@ struct lzk_event {
 
 extern "C" {
 
-const char* lzk_last_error(void) { return g_err.c_str(); }
+const char* lzk_last_error(void) { return lzk_detail::g_err.c_str(); }
 
 int lzk_device_count(int* count) {
   if (!count) return fail(LZK_ERR_INVALID, "null count");
@@ -384,7 +380,7 @@ int lzk_get_device(int* device) {
   return LZK_OK;
 }
 
-uint64_t lzk_kernel_launches(void) { return g_launches.load(); }
+uint64_t lzk_kernel_launches(void) { return lzk_detail::launches.load(); }
 
 int lzk_dev_alloc(int device, uint64_t bytes, void** ptr) {
   if (!ptr) return fail(LZK_ERR_INVALID, "null out pointer");
@@ -709,7 +705,7 @@ int lzk_fill_splitmix(lzk_stream* s, void* dev, uint64_t bytes, uint64_t seed, u
   uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>((words + 255) / 256, 148ull * 8));
   lzk_fill_kernel<<<grid, 256, 0, s->s>>>(static_cast<uint8_t*>(dev), bytes, seed, leaf);
   LZK_CK(cudaGetLastError());
-  g_launches.fetch_add(1, std::memory_order_relaxed);
+  lzk_detail::launches.fetch_add(1, std::memory_order_relaxed);
   return LZK_OK;
 }
 
@@ -718,7 +714,7 @@ int lzk_busy_compute(lzk_stream* s, float* buf, uint64_t n, uint32_t iters, uint
   if (int rc = use_device(s->device)) return rc;
   lzk_busy_kernel<<<ctas ? ctas : 148 * 4, 256, 0, s->s>>>(buf, n, iters);
   LZK_CK(cudaGetLastError());
-  g_launches.fetch_add(1, std::memory_order_relaxed);
+  lzk_detail::launches.fetch_add(1, std::memory_order_relaxed);
   return LZK_OK;
 }
 

@@ -1,0 +1,556 @@
+// B200 (sm_100a) FNV-1a-64 over many device byte ranges.
+//
+// The reference checksums every shard entry on the host, byte-serially
+// (include/lzckpt/checksum.hpp:17-24; folded per chunk in
+// src/flush_pipeline.cpp:194-263 and re-computed by the restore check in
+// src/format.cpp:173-214). One core folds ~0.7 GB/s, and the B200 hosts have
+// 16 cores for 8 GPUs that each snapshot at ~57 GB/s. This file computes the
+// same digests on the device, bit-exactly.
+//
+// Algorithm (executable model: tools/fnv_scan_model.py)
+//  * Step h' = (h ^ b) * P, P = 2^40 + 0x1b3. The low byte l = h & 0xff
+//    evolves on its own: l' = 0xb3 * (l ^ b) mod 256.
+//  * A 64-bit state whose low byte is right follows the true trajectory's
+//    low bytes, so plain FNV started from the value l gives
+//    acc = P^n * l + S, and the true state is h_end = P^n * h + (acc - P^n * l).
+//    A lane can therefore hash its own bytes independently once it knows the
+//    low byte at their start.
+//  * Those low bytes come from a bit-sliced scan. Multiplying by an odd
+//    constant is a T-function: bit i of 0xb3 * x is x_i xor a function of
+//    x_0..x_{i-1}. So plane i of the low-byte trajectory is a prefix-XOR of
+//    known bits once planes 0..i-1 are resolved. Each lane transposes its 32
+//    bytes into 8 bit-plane words. Per plane it runs an in-register prefix XOR
+//    (5 shift/xor steps), then a warp ballot + popc carries the parity across
+//    lanes and across 1 KiB windows. The column adder of y = x + 2x + 16x +
+//    32x + 128x supplies the lower-plane terms with a few LOP3s.
+//  * Per lane, two 16-byte FNV chains (low bytes at lane offsets 0 and 16)
+//    run interleaved. Lane results fold as R = R * P^1024 + window sum, and
+//    at the end h = P^(1024 C) h0 + sum_j R_j P^(32 (31 - j)).
+//
+// Two schedules:
+//  * short ranges: one warp per range (largest first, round-robin), one pass;
+//    about 16 integer ops per byte;
+//  * long ranges (more than a fair share of the grid, >= 4 MiB): split into
+//    up to 2048 segments of >= 256 KiB, all processed in parallel. Pass i
+//    (i = 0..7) gives every segment's plane-i parity, with the carry-in bits
+//    < i taken from the XOR of the earlier segments' parities (bit i of a
+//    segment's outgoing low byte depends only on incoming bits <= i). A final
+//    pass hashes every segment from its now-known incoming low byte, and one
+//    warp per range folds the segments affinely (h = P^len h + S). It costs
+//    about 4x the work of one pass, but one range can fill the GPU.
+#include <algorithm>
+#include <cstdint>
+#include <mutex>
+#include <numeric>
+#include <vector>
+
+#include "lzk_internal.h"
+
+namespace {
+
+using lzk_detail::cuda_fail;
+using lzk_detail::fail;
+using lzk_detail::use_device;
+
+constexpr uint64_t kPrime = 0x100000001b3ull;
+constexpr int kHashThreads = 512;
+constexpr int kHashWarps = kHashThreads / 32;
+constexpr uint64_t kSegMin = 256ull << 10;  // bytes, multiple of 1 KiB
+constexpr uint32_t kMaxSegs = 2048;         // per range
+constexpr uint64_t kLongMin = 4ull << 20;
+
+constexpr uint64_t cpow(uint64_t b, uint64_t e) {
+  uint64_t r = 1;
+  while (e) {
+    if (e & 1) r *= b;
+    b *= b;
+    e >>= 1;
+  }
+  return r;
+}
+constexpr uint64_t kP16 = cpow(kPrime, 16);
+constexpr uint64_t kP1024 = cpow(kPrime, 1024);
+
+struct HashItem {
+  lzk_hash_desc d;
+  uint32_t seg_begin;  // exclusive prefix of nseg over the batch
+  uint32_t nseg;       // 1 = short range (one warp, one pass)
+  uint64_t seglen;     // segment body bytes (multiple of 1 KiB) when nseg > 1
+};
+
+// The item table lives in device memory (any number of ranges per launch).
+struct HashBatch {
+  const HashItem* it;
+  uint32_t n;
+  uint32_t cont;        // 1: seeds are read from *out (continue a running digest)
+  uint32_t total_segs;
+  uint32_t pad;
+};
+
+__device__ __forceinline__ uint64_t pow64(uint64_t b, uint64_t e) {
+  uint64_t r = 1;
+  while (e) {
+    if (e & 1) r *= b;
+    b *= b;
+    e >>= 1;
+  }
+  return r;
+}
+
+__device__ __forceinline__ uint4 ld_nc(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ uint64_t fnv_word(uint64_t h, uint32_t w) {
+  h = (h ^ (w & 0xffu)) * kPrime;
+  h = (h ^ ((w >> 8) & 0xffu)) * kPrime;
+  h = (h ^ ((w >> 16) & 0xffu)) * kPrime;
+  h = (h ^ (w >> 24)) * kPrime;
+  return h;
+}
+
+__device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) {
+  return (a & b) | (a & c) | (b & c);
+}
+
+// o[t] = byte t of a, b, c, d (a 4x4 byte transpose in 8 PRMTs).
+__device__ __forceinline__ void bytes4x4(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t* o) {
+  const uint32_t ab_lo = __byte_perm(a, b, 0x5140), ab_hi = __byte_perm(a, b, 0x7362);
+  const uint32_t cd_lo = __byte_perm(c, d, 0x5140), cd_hi = __byte_perm(c, d, 0x7362);
+  o[0] = __byte_perm(ab_lo, cd_lo, 0x5410);
+  o[1] = __byte_perm(ab_lo, cd_lo, 0x7632);
+  o[2] = __byte_perm(ab_hi, cd_hi, 0x5410);
+  o[3] = __byte_perm(ab_hi, cd_hi, 0x7632);
+}
+
+__device__ __forceinline__ void delta_swap(uint32_t& a, uint32_t& b, uint32_t mask, int s) {
+  const uint32_t x = ((a >> s) ^ b) & mask;
+  b ^= x;
+  a ^= x << s;
+}
+
+// 32 bytes (w[q] holds bytes 4q..4q+3, little endian) -> 8 bit planes,
+// bit p of B[i] = bit i of byte p. A byte shuffle puts byte 8k+t in byte k
+// of word t, then three delta-swap stages transpose each byte lane's 8x8 bit
+// matrix across the eight words.
+__device__ __forceinline__ void to_planes(const uint32_t* w, uint32_t* B) {
+  bytes4x4(w[0], w[2], w[4], w[6], B);
+  bytes4x4(w[1], w[3], w[5], w[7], B + 4);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) delta_swap(B[t], B[t + 4], 0x0f0f0f0fu, 4);
+  delta_swap(B[0], B[2], 0x33333333u, 2);
+  delta_swap(B[1], B[3], 0x33333333u, 2);
+  delta_swap(B[4], B[6], 0x33333333u, 2);
+  delta_swap(B[5], B[7], 0x33333333u, 2);
+#pragma unroll
+  for (int t = 0; t < 8; t += 2) delta_swap(B[t], B[t + 1], 0x55555555u, 1);
+}
+
+// Low bytes of one warp window: lane j holds bytes [32j, 32j + 32) in w.
+// Resolves planes 0..NP-1. `carry` (warp-uniform) holds the low byte at the
+// window start and is advanced past it (bits < NP). `valid` masks the lane's
+// positions that exist (partial last window). Outputs the low bytes at the
+// lane's offsets 0 and 16 (meaningful when NP == 8).
+template <int NP>
+__device__ __forceinline__ void scan_planes(const uint32_t* w, uint32_t& carry, uint32_t lt, uint32_t valid,
+                                            uint32_t& l0, uint32_t& l16) {
+  uint32_t B[8];
+  to_planes(w, B);
+  uint32_t lstart = 0, lmid = 0;
+  // plane i: l_i at each position = carry-in xor exclusive prefix-XOR of
+  // e_i; returns x_i = l_i ^ b_i.
+  auto plane = [&](int i, uint32_t e) -> uint32_t {
+    uint32_t p = e & valid;
+    p ^= p << 1;
+    p ^= p << 2;
+    p ^= p << 4;
+    p ^= p << 8;
+    p ^= p << 16;
+    const uint32_t bal = __ballot_sync(0xffffffffu, p >> 31);
+    const uint32_t cin = (__popc(bal & lt) ^ (carry >> i)) & 1u;
+    carry ^= (__popc(bal) & 1u) << i;
+    const uint32_t l = (p << 1) ^ (0u - cin);
+    lstart |= cin << i;
+    lmid |= ((l >> 16) & 1u) << i;
+    return l ^ B[i];
+  };
+  // column adder of y = 179 x (mod 256): column i sums x_i, x_{i-1},
+  // x_{i-4}, x_{i-5}, x_{i-7} and the carries from column i-1.
+  const uint32_t x0 = plane(0, B[0]);
+  if constexpr (NP > 1) {
+    const uint32_t x1 = plane(1, B[1] ^ x0);
+    const uint32_t c2 = x1 & x0;
+    if constexpr (NP > 2) {
+      const uint32_t x2 = plane(2, B[2] ^ x1 ^ c2);
+      const uint32_t c3 = maj3(x2, x1, c2);
+      if constexpr (NP > 3) {
+        const uint32_t x3 = plane(3, B[3] ^ x2 ^ c3);
+        const uint32_t c4 = maj3(x3, x2, c3);
+        if constexpr (NP > 4) {
+          const uint32_t x4 = plane(4, B[4] ^ x3 ^ x0 ^ c4);
+          const uint32_t k1 = maj3(x4, x3, x0), k2 = (x4 ^ x3 ^ x0) & c4;
+          if constexpr (NP > 5) {
+            const uint32_t x5 = plane(5, B[5] ^ x4 ^ x1 ^ x0 ^ k1 ^ k2);
+            const uint32_t s1 = x5 ^ x4 ^ x1, m1 = maj3(x5, x4, x1);
+            const uint32_t s2 = x0 ^ k1 ^ k2, m2 = maj3(x0, k1, k2);
+            const uint32_t m3 = s1 & s2;
+            if constexpr (NP > 6) {
+              const uint32_t x6 = plane(6, B[6] ^ x5 ^ x2 ^ x1 ^ m1 ^ m2 ^ m3);
+              const uint32_t t1 = x6 ^ x5 ^ x2, n1 = maj3(x6, x5, x2);
+              const uint32_t t2 = x1 ^ m1 ^ m2, n2 = maj3(x1, m1, m2);
+              const uint32_t n3 = maj3(m3, t1, t2);
+              if constexpr (NP > 7) plane(7, B[7] ^ x6 ^ x3 ^ x2 ^ x0 ^ n1 ^ n2 ^ n3);
+            }
+          }
+        }
+      }
+    }
+  }
+  l0 = lstart;
+  l16 = lmid;
+}
+
+__device__ __forceinline__ uint64_t warp_sum(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ uint32_t head_len(uint64_t src, uint64_t len) {
+  const uint64_t h = (16u - (src & 15u)) & 15u;
+  return static_cast<uint32_t>(h < len ? h : len);
+}
+
+__device__ __forceinline__ uint64_t fold_bytes(uint64_t h, const uint8_t* p, uint32_t n) {
+  for (uint32_t i = 0; i < n; ++i) h = (h ^ p[i]) * kPrime;
+  return h;
+}
+
+// FNV-1a-64 of n bytes at p continuing from state h; all 32 lanes call it
+// with the same arguments and get the same result.
+__device__ uint64_t hash_range(const uint8_t* p, uint64_t n, uint64_t h, uint32_t lane, uint32_t lt,
+                               uint64_t wlane) {
+  const uint32_t head = head_len(reinterpret_cast<uintptr_t>(p), n);
+  h = fold_bytes(h, p, head);  // every lane, redundantly
+  p += head;
+  n -= head;
+
+  uint32_t carry = static_cast<uint32_t>(h) & 0xffu;
+  const uint64_t windows = n >> 10;
+  if (windows) {
+    const uint4* q = reinterpret_cast<const uint4*>(p) + 2 * lane;
+    uint4 a = ld_nc(q), b = ld_nc(q + 1);
+    uint64_t R = 0;
+    for (uint64_t c = 0; c < windows; ++c) {
+      const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      if (c + 1 < windows) {  // prefetch the next window
+        q += 64;
+        a = ld_nc(q);
+        b = ld_nc(q + 1);
+      }
+      uint32_t l0, l16;
+      scan_planes<8>(w, carry, lt, 0xffffffffu, l0, l16);
+      uint64_t a0 = l0, a1 = l16;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        a0 = fnv_word(a0, w[k]);
+        a1 = fnv_word(a1, w[k + 4]);
+      }
+      R = R * kP1024 + ((a0 - kP16 * l0) * kP16 + (a1 - kP16 * l16));
+    }
+    h = pow64(kP1024, windows) * h + warp_sum(R * wlane);
+  }
+
+  const uint32_t rem = static_cast<uint32_t>(n & 1023u);
+  if (rem) {
+    const uint8_t* t = p + (windows << 10) + 32u * lane;
+    const uint32_t cnt = rem > 32u * lane ? min(32u, rem - 32u * lane) : 0u;
+    uint32_t w[8];
+    if (cnt == 32) {
+      const uint4 a = ld_nc(reinterpret_cast<const uint4*>(t)), b = ld_nc(reinterpret_cast<const uint4*>(t) + 1);
+      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+      w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (uint32_t(4 * k + j) < cnt) v |= uint32_t(t[4 * k + j]) << (8 * j);
+        }
+        w[k] = v;
+      }
+    }
+    uint32_t l0, l16;
+    scan_planes<8>(w, carry, lt, cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u), l0, l16);
+    uint64_t acc = l0;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (uint32_t(k) < cnt) acc = (acc ^ ((w[k >> 2] >> (8 * (k & 3))) & 0xffu)) * kPrime;
+    }
+    uint64_t v = 0;
+    if (cnt) v = (acc - pow64(kPrime, cnt) * l0) * pow64(kPrime, rem - 32u * lane - cnt);
+    h = pow64(kPrime, rem) * h + warp_sum(v);
+  }
+  return h;
+}
+
+struct Scratch {
+  uint8_t* par;  // per segment: bit i = plane-i parity of the segment
+  uint64_t* S;   // per segment: true state after segment 0 / relative sum of the others
+};
+
+__device__ __forceinline__ uint32_t find_item(const HashBatch& b, uint32_t t) {
+  uint32_t lo = 0, hi = b.n - 1;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi + 1) >> 1;
+    if (b.it[mid].seg_begin <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ uint64_t item_seed(uint32_t cont, const HashItem& it) {
+  if (!cont) return it.d.seed;
+  uint64_t v;
+  asm volatile("ld.volatile.u64 %0, [%1];" : "=l"(v) : "l"(it.d.out));
+  return v;
+}
+
+// XOR of the parity bytes of segments [base, base + s): the low-byte
+// changes accumulated before segment s.
+__device__ __forceinline__ uint32_t parity_prefix(const uint8_t* par, uint32_t base, uint32_t s, uint32_t lane) {
+  uint32_t x = 0;
+  for (uint32_t k = lane; k < s; k += 32) x ^= par[base + k];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) x ^= __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// Pass I of the long-range schedule: plane-I parity of every segment that
+// has a successor.
+template <int I>
+__global__ void __launch_bounds__(kHashThreads) lzk_fnv_pass_kernel(const HashBatch batch, Scratch sc) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint32_t nwarps = gridDim.x * kHashWarps;
+  for (uint32_t t = blockIdx.x * kHashWarps + (threadIdx.x >> 5); t < batch.total_segs; t += nwarps) {
+    const HashItem it = batch.it[find_item(batch, t)];
+    const uint32_t s = t - it.seg_begin;
+    if (s + 1 >= it.nseg) continue;  // nobody consumes the last segment's parity
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(it.d.src);
+    const uint32_t head = head_len(it.d.src, it.d.len);
+    const uint64_t hh = fold_bytes(item_seed(batch.cont, it), src, head);
+    uint32_t carry = (static_cast<uint32_t>(hh) ^ parity_prefix(sc.par, it.seg_begin, s, lane)) & ((1u << I) - 1u);
+    const uint4* q = reinterpret_cast<const uint4*>(src + head + uint64_t(s) * it.seglen) + 2 * lane;
+    const uint64_t windows = it.seglen >> 10;
+    uint4 a = ld_nc(q), b = ld_nc(q + 1);
+    for (uint64_t c = 0; c < windows; ++c) {
+      const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      if (c + 1 < windows) {
+        q += 64;
+        a = ld_nc(q);
+        b = ld_nc(q + 1);
+      }
+      uint32_t l0, l16;
+      scan_planes<I + 1>(w, carry, lt, 0xffffffffu, l0, l16);
+    }
+    if (lane == 0) sc.par[t] |= static_cast<uint8_t>(carry & (1u << I));
+  }
+}
+
+// Final pass: short ranges are hashed whole (result stored to out); every
+// segment of a long range is hashed from its incoming low byte.
+__global__ void __launch_bounds__(kHashThreads) lzk_fnv_kernel(const HashBatch batch, Scratch sc) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint32_t nwarps = gridDim.x * kHashWarps;
+  const uint64_t wlane = pow64(kPrime, 32u * (31u - lane));
+  for (uint32_t t = blockIdx.x * kHashWarps + (threadIdx.x >> 5); t < batch.total_segs; t += nwarps) {
+    const HashItem it = batch.it[find_item(batch, t)];
+    const uint32_t s = t - it.seg_begin;
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(it.d.src);
+    const uint64_t h0 = item_seed(batch.cont, it);
+    if (it.nseg == 1) {
+      const uint64_t h = hash_range(src, it.d.len, h0, lane, lt, wlane);
+      if (lane == 0) *reinterpret_cast<uint64_t*>(it.d.out) = h;
+      continue;
+    }
+    const uint32_t head = head_len(it.d.src, it.d.len);
+    if (s == 0) {
+      const uint64_t h = hash_range(src, head + it.seglen, h0, lane, lt, wlane);
+      if (lane == 0) sc.S[t] = h;
+      continue;
+    }
+    const uint64_t off = head + uint64_t(s) * it.seglen;
+    const uint64_t n = min(it.seglen, it.d.len - off);
+    const uint32_t lin =
+        (static_cast<uint32_t>(fold_bytes(h0, src, head)) ^ parity_prefix(sc.par, it.seg_begin, s, lane)) & 0xffu;
+    const uint64_t acc = hash_range(src + off, n, lin, lane, lt, wlane);
+    if (lane == 0) sc.S[t] = acc - pow64(kPrime, n) * lin;
+  }
+}
+
+// h = S_0, then h = P^len_s * h + S_s over the remaining segments.
+__global__ void lzk_fnv_combine_kernel(const HashBatch batch, Scratch sc) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < batch.n; i += nwarps) {
+    const HashItem it = batch.it[i];
+    if (it.nseg == 1 || lane != 0) continue;
+    const uint64_t head = head_len(it.d.src, it.d.len);
+    const uint64_t pseg = pow64(kPrime, it.seglen);
+    uint64_t h = sc.S[it.seg_begin];
+    for (uint32_t s = 1; s < it.nseg; ++s) {
+      const uint64_t off = head + uint64_t(s) * it.seglen;
+      const uint64_t n = min(it.seglen, it.d.len - off);
+      h = (n == it.seglen ? pseg : pow64(kPrime, n)) * h + sc.S[it.seg_begin + s];
+    }
+    *reinterpret_cast<uint64_t*>(it.d.out) = h;
+  }
+}
+
+int sm_count(int device) {
+  static std::mutex mu;
+  static std::vector<int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  if (size_t(device) >= cache.size()) cache.resize(size_t(device) + 1, 0);
+  if (!cache[size_t(device)]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) n = 148;
+    cache[size_t(device)] = n;
+  }
+  return cache[size_t(device)];
+}
+
+template <int I>
+void launch_pass(uint32_t grid, cudaStream_t s, const HashBatch& b, Scratch sc) {
+  lzk_fnv_pass_kernel<I><<<grid, kHashThreads, 0, s>>>(b, sc);
+}
+
+// Pinned staging blocks of item tables, freed once the copy that reads them
+// has executed (checked on later calls).
+struct Staged {
+  void* host;
+  cudaEvent_t copied;
+};
+std::mutex g_stage_mu;
+std::vector<Staged> g_staged;
+
+void reap_staged() {
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  for (size_t i = 0; i < g_staged.size();) {
+    if (cudaEventQuery(g_staged[i].copied) == cudaSuccess) {
+      lzk_host_free(g_staged[i].host);
+      cudaEventDestroy(g_staged[i].copied);
+      g_staged[i] = g_staged.back();
+      g_staged.pop_back();
+    } else {
+      cudaGetLastError();  // clear cudaErrorNotReady
+      ++i;
+    }
+  }
+}
+
+int launch_hash(cudaStream_t stream, int device, const lzk_hash_desc* d, uint32_t n, uint32_t max_ctas, bool cont) {
+  if (n == 0) return LZK_OK;
+  if (d == nullptr) return fail(LZK_ERR_INVALID, "fnv: null descriptor array");
+  uint64_t total = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    if (d[i].out == 0) return fail(LZK_ERR_INVALID, "fnv: null output address");
+    if (d[i].src == 0 && d[i].len) return fail(LZK_ERR_INVALID, "fnv: null source");
+    total += d[i].len;
+  }
+  reap_staged();
+  const uint32_t ctas = max_ctas ? max_ctas : uint32_t(sm_count(device)) * 2;
+  const uint64_t fair = total / (uint64_t(ctas) * kHashWarps);
+  // largest first, dealt round-robin to warps (longest-processing-time order)
+  std::vector<uint32_t> order(n);
+  std::iota(order.begin(), order.end(), 0u);
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return d[a].len > d[b].len; });
+  void* host = nullptr;
+  if (int rc = lzk_host_alloc(uint64_t(n) * sizeof(HashItem), 0, &host)) return rc;
+  HashItem* items = static_cast<HashItem*>(host);
+  uint32_t segs = 0;
+  bool any_long = false;
+  for (uint32_t i = 0; i < n; ++i) {
+    HashItem& it = items[i];
+    it.d = d[order[i]];
+    it.seg_begin = segs;
+    it.nseg = 1;
+    it.seglen = 0;
+    const uint64_t body = it.d.len - std::min<uint64_t>(it.d.len, (16u - (it.d.src & 15u)) & 15u);
+    if (it.d.len >= kLongMin && it.d.len > 2 * fair) {
+      uint64_t sl = std::max<uint64_t>(kSegMin, (body + kMaxSegs - 1) / kMaxSegs);
+      sl = (sl + 1023) & ~uint64_t(1023);
+      const uint64_t ns = (body + sl - 1) / sl;
+      if (ns > 1) {
+        it.nseg = uint32_t(ns);
+        it.seglen = sl;
+        any_long = true;
+      }
+    }
+    segs += it.nseg;
+  }
+  // device block: item table, then (long ranges) per-segment sums and parities
+  const uint64_t table = (uint64_t(n) * sizeof(HashItem) + 255) & ~uint64_t(255);
+  const uint64_t bytes = table + (any_long ? uint64_t(segs) * 9 + 16 : 0);
+  void* dev = nullptr;
+  cudaEvent_t copied = nullptr;
+  cudaError_t e = cudaMallocAsync(&dev, bytes, stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dev, host, uint64_t(n) * sizeof(HashItem), cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&copied, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(copied, stream);
+  if (e != cudaSuccess) {
+    cudaStreamSynchronize(stream);
+    lzk_host_free(host);
+    if (copied) cudaEventDestroy(copied);
+    return cuda_fail(e, "fnv: item table");
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_stage_mu);
+    g_staged.push_back({host, copied});
+  }
+  HashBatch batch{static_cast<const HashItem*>(dev), n, cont ? 1u : 0u, segs, 0};
+  Scratch sc{nullptr, nullptr};
+  if (any_long) {
+    sc.S = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(dev) + table);
+    sc.par = reinterpret_cast<uint8_t*>(sc.S + segs);
+    LZK_CK(cudaMemsetAsync(sc.par, 0, segs, stream));
+  }
+  const uint32_t grid = std::max(1u, std::min<uint32_t>((segs + kHashWarps - 1) / kHashWarps, ctas));
+  if (any_long) {
+    launch_pass<0>(grid, stream, batch, sc);
+    launch_pass<1>(grid, stream, batch, sc);
+    launch_pass<2>(grid, stream, batch, sc);
+    launch_pass<3>(grid, stream, batch, sc);
+    launch_pass<4>(grid, stream, batch, sc);
+    launch_pass<5>(grid, stream, batch, sc);
+    launch_pass<6>(grid, stream, batch, sc);
+    launch_pass<7>(grid, stream, batch, sc);
+  }
+  lzk_fnv_kernel<<<grid, kHashThreads, 0, stream>>>(batch, sc);
+  if (any_long) lzk_fnv_combine_kernel<<<(n + 7) / 8, 256, 0, stream>>>(batch, sc);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "lzk_fnv kernels launch");
+  lzk_detail::launches.fetch_add(any_long ? 10 : 1, std::memory_order_relaxed);
+  LZK_CK(cudaFreeAsync(dev, stream));
+  return LZK_OK;
+}
+
+}  // namespace
+
+extern "C" int lzk_fnv1a64_batch(lzk_stream* s, const lzk_hash_desc* d, uint32_t n, uint32_t max_ctas) {
+  if (!s) return fail(LZK_ERR_INVALID, "null stream");
+  if (int rc = use_device(s->device)) return rc;
+  return launch_hash(s->s, s->device, d, n, max_ctas, false);
+}
+
+extern "C" int lzk_fnv1a64_continue(lzk_stream* s, const lzk_hash_desc* d, uint32_t n, uint32_t max_ctas) {
+  if (!s) return fail(LZK_ERR_INVALID, "null stream");
+  if (int rc = use_device(s->device)) return rc;
+  return launch_hash(s->s, s->device, d, n, max_ctas, true);
+}

@@ -736,6 +736,39 @@ def kernel_launches() -> int:
     return dev.lzk_kernel_launches()
 
 
+FNV_BASIS = 0xCBF29CE484222325
+
+
+def _dev_check(rc: int) -> None:
+    if rc != 0:
+        raise (InvalidArgument if rc == 1 else DeviceError)(dev.lzk_last_error().decode(errors="replace"))
+
+
+def device_fnv64(ranges: Sequence[Tuple[int, int]], device: int = 0, seeds: Optional[Sequence[int]] = None,
+                 max_ctas: int = 0) -> List[int]:
+    """FNV-1a-64 of device byte ranges [(address, length), ...] computed on
+    the GPU (lzk_fnv1a64_batch), bit-identical to fnv64() of the same bytes;
+    `seeds` continues from given states instead of the FNV basis."""
+    n = len(ranges)
+    if n == 0:
+        return []
+    out = C.c_void_p()
+    _dev_check(dev.lzk_host_alloc(8 * n, 1, C.byref(out)))
+    s = C.c_void_p()
+    try:
+        _dev_check(dev.lzk_stream_create(device, 0, C.byref(s)))
+        arr = (N.HashDescC * n)()
+        for i, (ptr, ln) in enumerate(ranges):
+            arr[i] = N.HashDescC(ptr, ln, FNV_BASIS if seeds is None else seeds[i], out.value + 8 * i)
+        _dev_check(dev.lzk_fnv1a64_batch(s, arr, n, max_ctas))
+        _dev_check(dev.lzk_stream_sync(s))
+        return list((C.c_uint64 * n).from_address(out.value))
+    finally:
+        if s.value:
+            dev.lzk_stream_destroy(s)
+        dev.lzk_host_free(out)
+
+
 @dataclasses.dataclass
 class BuiltWorkload:
     tree: StateTree
