@@ -58,6 +58,10 @@ class DeviceRegion {
 
   // Non-owning view of memory someone else allocated (e.g. a torch tensor).
   static std::shared_ptr<DeviceRegion> wrap(void* device_ptr, uint64_t size, int device);
+  // Same, keeping `owner` (e.g. a block several regions are carved from)
+  // alive for as long as the region lives.
+  static std::shared_ptr<DeviceRegion> wrap(void* device_ptr, uint64_t size, int device,
+                                            std::shared_ptr<void> owner);
 
   uint64_t size() const { return size_; }
   uint64_t version() const { return version_.load(std::memory_order_acquire); }

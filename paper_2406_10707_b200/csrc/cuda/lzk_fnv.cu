@@ -82,7 +82,7 @@ struct HashItem {
 struct HashBatch {
   const HashItem* it;
   uint32_t n;
-  uint32_t cont;        // 1: seeds are read from *out (continue a running digest)
+  uint32_t pad0;
   uint32_t total_segs;
   uint32_t pad;
 };
@@ -313,11 +313,26 @@ __device__ __forceinline__ uint32_t find_item(const HashBatch& b, uint32_t t) {
   return lo;
 }
 
-__device__ __forceinline__ uint64_t item_seed(uint32_t cont, const HashItem& it) {
-  if (!cont) return it.d.seed;
-  uint64_t v;
-  asm volatile("ld.volatile.u64 %0, [%1];" : "=l"(v) : "l"(it.d.out));
-  return v;
+// Items reach the device through kernel parameters: each upload launch
+// carries up to kUploadItems of them and writes them into the device table
+// (no pinned staging, no host-side allocation per call). In continue mode
+// the running state is read from *out (often mapped host memory) here, once
+// per item, so no hashing warp ever reads its seed across PCIe.
+constexpr uint32_t kUploadItems = 600;
+struct UploadParams {
+  HashItem* dst;
+  uint32_t n;
+  uint32_t cont;
+  HashItem items[kUploadItems];
+};
+static_assert(sizeof(UploadParams) <= 31 * 1024, "kernel parameter budget");
+
+__global__ void lzk_fnv_upload_kernel(const __grid_constant__ UploadParams p) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.n) return;
+  HashItem it = p.items[i];
+  if (p.cont) asm volatile("ld.volatile.u64 %0, [%1];" : "=l"(it.d.seed) : "l"(it.d.out));
+  p.dst[i] = it;
 }
 
 // XOR of the parity bytes of segments [base, base + s): the low-byte
@@ -343,7 +358,7 @@ __global__ void __launch_bounds__(kHashThreads) lzk_fnv_pass_kernel(const HashBa
     if (s + 1 >= it.nseg) continue;  // nobody consumes the last segment's parity
     const uint8_t* src = reinterpret_cast<const uint8_t*>(it.d.src);
     const uint32_t head = head_len(it.d.src, it.d.len);
-    const uint64_t hh = fold_bytes(item_seed(batch.cont, it), src, head);
+    const uint64_t hh = fold_bytes(it.d.seed, src, head);
     uint32_t carry = (static_cast<uint32_t>(hh) ^ parity_prefix(sc.par, it.seg_begin, s, lane)) & ((1u << I) - 1u);
     const uint4* q = reinterpret_cast<const uint4*>(src + head + uint64_t(s) * it.seglen) + 2 * lane;
     const uint64_t windows = it.seglen >> 10;
@@ -373,7 +388,7 @@ __global__ void __launch_bounds__(kHashThreads) lzk_fnv_kernel(const HashBatch b
     const HashItem it = batch.it[find_item(batch, t)];
     const uint32_t s = t - it.seg_begin;
     const uint8_t* src = reinterpret_cast<const uint8_t*>(it.d.src);
-    const uint64_t h0 = item_seed(batch.cont, it);
+    const uint64_t h0 = it.d.seed;
     if (it.nseg == 1) {
       const uint64_t h = hash_range(src, it.d.len, h0, lane, lt, wlane);
       if (lane == 0) *reinterpret_cast<uint64_t*>(it.d.out) = h;
@@ -431,28 +446,21 @@ void launch_pass(uint32_t grid, cudaStream_t s, const HashBatch& b, Scratch sc) 
   lzk_fnv_pass_kernel<I><<<grid, kHashThreads, 0, s>>>(b, sc);
 }
 
-// Pinned staging blocks of item tables, freed once the copy that reads them
-// has executed (checked on later calls).
-struct Staged {
-  void* host;
-  cudaEvent_t copied;
-};
-std::mutex g_stage_mu;
-std::vector<Staged> g_staged;
-
-void reap_staged() {
-  std::lock_guard<std::mutex> lk(g_stage_mu);
-  for (size_t i = 0; i < g_staged.size();) {
-    if (cudaEventQuery(g_staged[i].copied) == cudaSuccess) {
-      lzk_host_free(g_staged[i].host);
-      cudaEventDestroy(g_staged[i].copied);
-      g_staged[i] = g_staged.back();
-      g_staged.pop_back();
-    } else {
-      cudaGetLastError();  // clear cudaErrorNotReady
-      ++i;
-    }
+void set_pool_threshold(int device) {
+  // Keep freed stream-ordered scratch in the device's default pool between
+  // calls instead of returning it to the OS at every synchronization.
+  static std::mutex mu;
+  static std::vector<bool> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (size_t(device) >= done.size()) done.resize(size_t(device) + 1, false);
+  if (done[size_t(device)]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = 1ull << 30;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
   }
+  cudaGetLastError();
+  done[size_t(device)] = true;
 }
 
 int launch_hash(cudaStream_t stream, int device, const lzk_hash_desc* d, uint32_t n, uint32_t max_ctas, bool cont) {
@@ -464,16 +472,14 @@ int launch_hash(cudaStream_t stream, int device, const lzk_hash_desc* d, uint32_
     if (d[i].src == 0 && d[i].len) return fail(LZK_ERR_INVALID, "fnv: null source");
     total += d[i].len;
   }
-  reap_staged();
+  set_pool_threshold(device);
   const uint32_t ctas = max_ctas ? max_ctas : uint32_t(sm_count(device)) * 2;
   const uint64_t fair = total / (uint64_t(ctas) * kHashWarps);
   // largest first, dealt round-robin to warps (longest-processing-time order)
   std::vector<uint32_t> order(n);
   std::iota(order.begin(), order.end(), 0u);
   std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return d[a].len > d[b].len; });
-  void* host = nullptr;
-  if (int rc = lzk_host_alloc(uint64_t(n) * sizeof(HashItem), 0, &host)) return rc;
-  HashItem* items = static_cast<HashItem*>(host);
+  std::vector<HashItem> items(n);
   uint32_t segs = 0;
   bool any_long = false;
   for (uint32_t i = 0; i < n; ++i) {
@@ -495,26 +501,23 @@ int launch_hash(cudaStream_t stream, int device, const lzk_hash_desc* d, uint32_
     }
     segs += it.nseg;
   }
-  // device block: item table, then (long ranges) per-segment sums and parities
+  // stream-ordered device block: item table, then (long ranges) per-segment
+  // sums and parities
   const uint64_t table = (uint64_t(n) * sizeof(HashItem) + 255) & ~uint64_t(255);
   const uint64_t bytes = table + (any_long ? uint64_t(segs) * 9 + 16 : 0);
   void* dev = nullptr;
-  cudaEvent_t copied = nullptr;
-  cudaError_t e = cudaMallocAsync(&dev, bytes, stream);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(dev, host, uint64_t(n) * sizeof(HashItem), cudaMemcpyHostToDevice, stream);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&copied, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventRecord(copied, stream);
-  if (e != cudaSuccess) {
-    cudaStreamSynchronize(stream);
-    lzk_host_free(host);
-    if (copied) cudaEventDestroy(copied);
-    return cuda_fail(e, "fnv: item table");
+  LZK_CK(cudaMallocAsync(&dev, bytes, stream));
+  uint32_t launches = 0;
+  thread_local UploadParams up;
+  for (uint32_t i = 0; i < n; i += kUploadItems) {
+    up.dst = static_cast<HashItem*>(dev) + i;
+    up.n = std::min(kUploadItems, n - i);
+    up.cont = cont ? 1u : 0u;
+    std::copy(items.begin() + i, items.begin() + i + up.n, up.items);
+    lzk_fnv_upload_kernel<<<(up.n + 127) / 128, 128, 0, stream>>>(up);
+    ++launches;
   }
-  {
-    std::lock_guard<std::mutex> lk(g_stage_mu);
-    g_staged.push_back({host, copied});
-  }
-  HashBatch batch{static_cast<const HashItem*>(dev), n, cont ? 1u : 0u, segs, 0};
+  HashBatch batch{static_cast<const HashItem*>(dev), n, 0, segs, 0};
   Scratch sc{nullptr, nullptr};
   if (any_long) {
     sc.S = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(dev) + table);
@@ -531,12 +534,17 @@ int launch_hash(cudaStream_t stream, int device, const lzk_hash_desc* d, uint32_
     launch_pass<5>(grid, stream, batch, sc);
     launch_pass<6>(grid, stream, batch, sc);
     launch_pass<7>(grid, stream, batch, sc);
+    launches += 8;
   }
   lzk_fnv_kernel<<<grid, kHashThreads, 0, stream>>>(batch, sc);
-  if (any_long) lzk_fnv_combine_kernel<<<(n + 7) / 8, 256, 0, stream>>>(batch, sc);
-  e = cudaGetLastError();
+  ++launches;
+  if (any_long) {
+    lzk_fnv_combine_kernel<<<(n + 7) / 8, 256, 0, stream>>>(batch, sc);
+    ++launches;
+  }
+  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "lzk_fnv kernels launch");
-  lzk_detail::launches.fetch_add(any_long ? 10 : 1, std::memory_order_relaxed);
+  lzk_detail::launches.fetch_add(launches, std::memory_order_relaxed);
   LZK_CK(cudaFreeAsync(dev, stream));
   return LZK_OK;
 }

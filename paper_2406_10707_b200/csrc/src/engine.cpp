@@ -44,6 +44,8 @@ double since(std::chrono::steady_clock::time_point t0) {
 
 // LZCKPT_TRACE=1: per-phase capture timing on stderr (host-overhead tuning).
 struct PhaseTrace {
+  explicit PhaseTrace(const char* what = "capture") : what(what) {}
+  const char* what;
   bool on = std::getenv("LZCKPT_TRACE") != nullptr;
   std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
   std::string line;
@@ -54,7 +56,7 @@ struct PhaseTrace {
     t = now;
   }
   ~PhaseTrace() {
-    if (on) std::fprintf(stderr, "[lzckpt capture ms]%s\n", line.c_str());
+    if (on) std::fprintf(stderr, "[lzckpt %s ms]%s\n", what, line.c_str());
   }
 };
 
@@ -89,8 +91,6 @@ struct Pinned {
     cap = n;
   }
 };
-
-unsigned io_threads() { return std::clamp(std::thread::hardware_concurrency(), 2u, 16u); }
 
 // Runs fn(i) for i in [0, n) on up to `threads` threads.
 template <class Fn>
@@ -709,18 +709,21 @@ struct EntrySink {
   std::vector<std::byte>* host = nullptr; // a host buffer (blobs, __meta__)
 };
 
-// Streams one committed shard file through a few pinned windows: a reader
-// thread preads window i+1 while window i is hashed (FNV-1a per entry,
-// continued across windows; different entries of a window in parallel) and
-// DMA'd into its sinks. Memory stays bounded by the windows whatever the file
-// size (C2's optimizer file is 84 GB). Returns the keys whose checksum
-// mismatches (the caller decides what that voids).
+// Streams one committed shard file through a few pinned windows. A reader
+// thread preads window i+1 while window i goes to HBM in one DMA; there its
+// entry slices are checksummed on the GPU (lzk_fnv1a64_continue: per-entry
+// FNV-1a states continued across windows, kept in mapped host memory) and
+// scattered device-to-device into their device sinks; host sinks are copied
+// from the pinned window. No byte is hashed on the host. Memory stays bounded
+// by the windows whatever the file size (C2's optimizer file is 84 GB).
+// Returns the keys whose checksum mismatches (the caller decides what that
+// voids).
 class FileStreamer {
  public:
   static constexpr uint64_t kWindow = 512ull << 20;
   static constexpr int kWindows = 3;
 
-  FileStreamer(int device, uint64_t ce_threshold) : device_(device), ce_threshold_(ce_threshold) {
+  FileStreamer(int device, uint64_t /*ce_threshold*/) : device_(device) {
     ck(lzk_stream_create(device, 0, &stream_), "restore stream");
     for (auto& w : win_) ck(lzk_event_create(device, 1, &w.done), "restore event");
   }
@@ -728,12 +731,15 @@ class FileStreamer {
     for (auto& w : win_) {
       if (w.done) lzk_event_destroy(w.done);
       lzk_host_free(w.buf);
+      lzk_dev_free(device_, w.dbuf);
     }
+    lzk_host_free(states_);
     lzk_stream_destroy(stream_);
   }
 
   std::vector<std::string> run(const std::filesystem::path& path, const CheckpointFileHeader& h,
                                const std::vector<EntrySink>& sinks) {
+    PhaseTrace tr("restore_stream");
     const uint64_t hsize = h.serialized_size(), end = h.payload_end();
     const int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
     if (fd < 0) throw IoError("cannot open " + path.string());
@@ -748,14 +754,32 @@ class FileStreamer {
       Window& w = win_[k];
       if (k < slots && w.cap < wsize) {
         lzk_host_free(w.buf);
+        w.buf = nullptr;
+        lzk_dev_free(device_, w.dbuf);
+        w.dbuf = nullptr;
         void* p = nullptr;
         ck(lzk_host_alloc(wsize, LZK_HOST_MAPPED | LZK_HOST_HUGEPAGE, &p), "restore window");
         w.buf = static_cast<std::byte*>(p);
+        tr.mark("host_window");
+        ck(lzk_dev_alloc(device_, wsize, &p), "restore device window");
+        w.dbuf = static_cast<std::byte*>(p);
+        tr.mark("dev_window");
         w.cap = wsize;
       }
       w.used = false;
     }
-    std::vector<uint64_t> state(h.entries.size(), Fnv64::kOffset);
+    // per-entry running digests, written by the GPU
+    const size_t ne = h.entries.size();
+    if (states_cap_ < ne) {
+      lzk_host_free(states_);
+      void* p = nullptr;
+      ck(lzk_host_alloc(std::max<size_t>(ne, 1) * 8, LZK_HOST_MAPPED, &p), "restore digests");
+      states_ = static_cast<uint64_t*>(p);
+      states_cap_ = ne;
+    }
+    for (size_t e = 0; e < ne; ++e) states_[e] = Fnv64::kOffset;
+    tr.mark("setup");
+    double wait_read = 0, t_h2d = 0, t_hash = 0, t_d2d = 0;
     const size_t nwin = size_t((n + wsize - 1) / wsize);
     // reader: window i -> slot i % kWindows (waits until the slot's DMA finished)
     auto read_window = [&](size_t i) {
@@ -771,9 +795,18 @@ class FileStreamer {
     std::thread reader;
     std::exception_ptr read_err;
     if (nwin) read_window(0);
+    tr.mark("read0");
     for (size_t i = 0; i < nwin; ++i) {
+      const auto tw = std::chrono::steady_clock::now();
       if (reader.joinable()) reader.join();
+      wait_read += since(tw);
       if (read_err) std::rethrow_exception(read_err);
+      Window& w = win_[i % kWindows];
+      const uint64_t off = uint64_t(i) * wsize, len = std::min(wsize, n - off);
+      lzk_copy_desc up{reinterpret_cast<uint64_t>(w.buf), reinterpret_cast<uint64_t>(w.dbuf), len};
+      ck(lzk_ce_copy_h2d(stream_, &up, 1), "restore DMA");
+      ck(lzk_event_record(w.done, stream_), "restore event");  // host window reusable after this
+      w.used = true;
       if (i + 1 < nwin) {
         reader = std::thread([&, i] {
           try {
@@ -783,61 +816,64 @@ class FileStreamer {
           }
         });
       }
-      Window& w = win_[i % kWindows];
-      const uint64_t off = uint64_t(i) * wsize, len = std::min(wsize, n - off);
       // entry slices overlapping [off, off + len) of the payload
-      struct Slice {
-        size_t e;
-        uint64_t a, b;  // payload-relative
-      };
-      std::vector<Slice> sl;
-      for (size_t e = 0; e < h.entries.size(); ++e) {
+      std::vector<lzk_hash_desc> hd;
+      std::vector<lzk_copy_desc> d2d;
+      for (size_t e = 0; e < ne; ++e) {
         const uint64_t eb = h.entries[e].offset - hsize, ee = eb + h.entries[e].length;
         const uint64_t a = std::max(eb, off), b = std::min(ee, off + len);
-        if (a < b) sl.push_back({e, a, b});
-      }
-      std::vector<lzk_copy_desc> ce, small;
-      for (const auto& x : sl) {
-        const EntrySink& s = sinks[x.e];
-        const uint64_t eb = h.entries[x.e].offset - hsize;
+        if (a >= b) continue;
+        const uint64_t src = reinterpret_cast<uint64_t>(w.dbuf + (a - off));
+        hd.push_back({src, b - a, 0, reinterpret_cast<uint64_t>(states_ + e)});
+        const EntrySink& s = sinks[e];
         if (s.device) {
-          lzk_copy_desc d{reinterpret_cast<uint64_t>(w.buf + (x.a - off)),
-                          reinterpret_cast<uint64_t>(static_cast<std::byte*>(s.device) + (x.a - eb)), x.b - x.a};
-          (h.entries[x.e].length >= ce_threshold_ ? ce : small).push_back(d);
+          d2d.push_back({src, reinterpret_cast<uint64_t>(static_cast<std::byte*>(s.device) + (a - eb)), b - a});
         } else if (s.host) {
-          std::memcpy(s.host->data() + (x.a - eb), w.buf + (x.a - off), x.b - x.a);
+          std::memcpy(s.host->data() + (a - eb), w.buf + (a - off), b - a);
         }
       }
-      if (!small.empty()) ck(lzk_scatter_h2d(stream_, small.data(), uint32_t(small.size()), 0), "restore scatter");
-      if (!ce.empty()) ck(lzk_ce_copy_h2d(stream_, ce.data(), uint32_t(ce.size())), "restore DMA");
-      ck(lzk_event_record(w.done, stream_), "restore event");
-      w.used = true;
-      parallel_for(sl.size(), io_threads(), [&](size_t k) {
-        const Slice& x = sl[k];
-        state[x.e] = Fnv64::fold(state[x.e], w.buf + (x.a - off), x.b - x.a);
-      });
+      auto gpu_mark = [&](double& acc) {  // trace only: serializes the pipeline
+        if (!tr.on) return;
+        const auto t0 = std::chrono::steady_clock::now();
+        ck(lzk_stream_sync(stream_), "restore trace sync");
+        acc += since(t0);
+      };
+      gpu_mark(t_h2d);
+      if (!hd.empty()) ck(lzk_fnv1a64_continue(stream_, hd.data(), uint32_t(hd.size()), 0), "restore checksums");
+      gpu_mark(t_hash);
+      if (!d2d.empty()) ck(lzk_gather_d2d(stream_, d2d.data(), uint32_t(d2d.size()), 0), "restore scatter");
+      gpu_mark(t_d2d);
     }
     if (reader.joinable()) reader.join();
     if (read_err) std::rethrow_exception(read_err);
+    tr.mark("windows");
     ck(lzk_stream_sync(stream_), "restore sync");
+    tr.mark("sync");
+    if (tr.on) {
+      tr.line += " read_wait=" + std::to_string(wait_read * 1e3) + " h2d=" + std::to_string(t_h2d * 1e3) +
+                 " hash=" + std::to_string(t_hash * 1e3) + " d2d=" + std::to_string(t_d2d * 1e3) +
+                 " nwin=" + std::to_string(nwin);
+    }
     std::vector<std::string> bad;
-    for (size_t e = 0; e < h.entries.size(); ++e) {
-      if (state[e] != h.entries[e].checksum) bad.push_back(h.entries[e].key);
+    for (size_t e = 0; e < ne; ++e) {
+      if (states_[e] != h.entries[e].checksum) bad.push_back(h.entries[e].key);
     }
     return bad;
   }
 
  private:
   struct Window {
-    std::byte* buf = nullptr;
+    std::byte* buf = nullptr;   // pinned host
+    std::byte* dbuf = nullptr;  // device copy of the window
     uint64_t cap = 0;
     lzk_event* done = nullptr;
     bool used = false;
   };
   int device_;
-  uint64_t ce_threshold_;
   lzk_stream* stream_ = nullptr;
   Window win_[kWindows];
+  uint64_t* states_ = nullptr;
+  size_t states_cap_ = 0;
 };
 
 // Header + exact-extent check (reference read_header + validate_entries
@@ -879,24 +915,45 @@ namespace {
 // blobs and inline leaves from host bytes. Reads each byte once.
 void restore_one(const std::filesystem::path& path, StateTree& tree, const StateTree* into, int dev,
                  FileStreamer& streamer) {
+  PhaseTrace tr("restore_one");
   CheckpointFileHeader h;
   auto leaves = open_shard(path, h);
+  tr.mark("open_shard");
   std::vector<EntrySink> sinks(h.entries.size());
   std::vector<std::vector<std::byte>> hostbufs(h.entries.size());
   std::vector<std::shared_ptr<DeviceRegion>> regions(leaves.size());
-  auto region_for = [&](const LeafManifestEntry& l) {
+  auto reuse = [&](const LeafManifestEntry& l) -> std::shared_ptr<DeviceRegion> {
     if (into && into->has(l.path)) {
       try {
         auto r = into->region_at(l.path);
-        if (r->size() == l.size && r->device() == dev) {
-          r->bump_version();  // contents are being replaced
-          return r;
-        }
+        if (r->size() == l.size && r->device() == dev) return r;
       } catch (const Error&) {
-        // a blob at that path: fall through to a fresh region
+        // a blob at that path: a fresh region instead
       }
     }
-    return std::make_shared<DeviceRegion>(DeviceRegion::Uninitialized{}, l.size, dev);
+    return nullptr;
+  };
+  // Fresh regions are carved from one device block per file (one allocation
+  // instead of one per tensor); the block lives as long as any of them.
+  uint64_t fresh = 0;
+  for (const auto& l : leaves) {
+    if (l.is_region && !reuse(l)) fresh += (l.size + 255) & ~uint64_t(255);
+  }
+  std::shared_ptr<void> block;
+  if (fresh) {
+    void* p = nullptr;
+    ck(lzk_dev_alloc(dev, fresh, &p), "restore: device allocation");
+    block = std::shared_ptr<void>(p, [dev](void* q) { lzk_dev_free(dev, q); });
+  }
+  uint64_t carved = 0;
+  auto region_for = [&](const LeafManifestEntry& l) {
+    if (auto r = reuse(l)) {
+      r->bump_version();  // contents are being replaced
+      return r;
+    }
+    void* p = static_cast<std::byte*>(block.get()) + carved;
+    carved += (l.size + 255) & ~uint64_t(255);
+    return DeviceRegion::wrap(p, l.size, dev, block);
   };
   for (size_t e = 0; e < h.entries.size(); ++e) {
     if (h.entries[e].key == StateTree::kMetaKey) {
@@ -922,7 +979,9 @@ void restore_one(const std::filesystem::path& path, StateTree& tree, const State
       sinks[e].host = &hostbufs[e];
     }
   }
+  tr.mark("regions");
   throw_bad(path, streamer.run(path, h, sinks));
+  tr.mark("stream");
   std::vector<lzk_copy_desc> inl;
   Pinned stage;
   uint64_t inline_total = 0;
@@ -958,6 +1017,7 @@ void restore_one(const std::filesystem::path& path, StateTree& tree, const State
     lzk_stream_destroy(s);
     ck(rc, "restore inline leaves");
   }
+  tr.mark("inline");
 }
 
 }  // namespace

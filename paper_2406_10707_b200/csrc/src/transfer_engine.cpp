@@ -64,6 +64,13 @@ std::shared_ptr<DeviceRegion> DeviceRegion::wrap(void* device_ptr, uint64_t size
   return std::shared_ptr<DeviceRegion>(new DeviceRegion(WrapTag{}, device_ptr, size, resolve_device(device)));
 }
 
+std::shared_ptr<DeviceRegion> DeviceRegion::wrap(void* device_ptr, uint64_t size, int device,
+                                                 std::shared_ptr<void> owner) {
+  if (!device_ptr && size) throw Error("DeviceRegion::wrap: null device pointer");
+  auto* r = new DeviceRegion(WrapTag{}, device_ptr, size, resolve_device(device));
+  return std::shared_ptr<DeviceRegion>(r, [owner = std::move(owner)](DeviceRegion* x) { delete x; });
+}
+
 DeviceRegion::~DeviceRegion() {
   if (owned_ && ptr_) lzk_dev_free(device_, ptr_);
 }

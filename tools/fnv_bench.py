@@ -73,8 +73,45 @@ def run(name, sizes, ctas_list):
               flush=True)
 
 
-c2 = [sz for kind, _, sz in llama7b_shard().leaves if kind == "r"]
-run("c2", c2, [1, 2, 4, 8, 16, 32, 64, 148, 0])
-run("uniform", [1 << 20] * 4096, [1, 8, 16, 148, 0])
-run("single", [1 << 30], [1, 16, 148, 0])
-run("window", [300 << 20, 212 << 20], [16, 148, 0])
+if not os.environ.get("FNV_BENCH_ONLY_CONT"):
+    c2 = [sz for kind, _, sz in llama7b_shard().leaves if kind == "r"]
+    run("c2", c2, [1, 2, 4, 8, 16, 32, 64, 148, 0])
+    run("uniform", [1 << 20] * 4096, [1, 8, 16, 148, 0])
+    run("single", [1 << 30], [1, 16, 148, 0])
+    run("window", [300 << 20, 212 << 20], [16, 148, 0])
+
+
+def run_cont(name, sizes, mapped, cont, ctas=0, odd=True):
+    """Restore-like call: slices at odd offsets, states in mapped host or
+    device memory, continue mode."""
+    st = C.c_void_p()
+    if mapped:
+        ck(d.lzk_host_alloc(8 * len(sizes), 1, C.byref(st)))
+    else:
+        ck(d.lzk_dev_alloc(0, 8 * len(sizes), C.byref(st)))
+    arr = (N.HashDescC * len(sizes))()
+    off = 5 if odd else 0
+    for i, n in enumerate(sizes):
+        arr[i] = N.HashDescC(p.value + off, n, lz.FNV_BASIS, st.value + 8 * i)
+        off += n
+    fn = d.lzk_fnv1a64_continue if cont else d.lzk_fnv1a64_batch
+    best = None
+    for _ in range(3):
+        ck(d.lzk_event_record(e0, s))
+        ck(fn(s, arr, len(sizes), ctas))
+        ck(d.lzk_event_record(e1, s))
+        ck(d.lzk_stream_sync(s))
+        ms = C.c_float()
+        ck(d.lzk_event_elapsed_ms(e0, e1, C.byref(ms)))
+        best = ms.value if best is None else min(best, ms.value)
+    print(json.dumps({"case": name, "mapped_out": mapped, "continue": cont, "odd": odd, "entries": len(sizes),
+                      "bytes": sum(sizes), "ms": round(best, 3), "GBps": round(sum(sizes) / best / 1e6, 2)}),
+          flush=True)
+
+
+if os.environ.get("FNV_BENCH_ONLY_CONT"):
+    sl = [67108864 - 1000, 67108864, 67108864 + 3, 67108864, 67108864, 67108864, 67108864, 67108864 - 7000]
+    for mapped in (False, True):
+        for cont in (False, True):
+            run_cont("restore_window", sl, mapped, cont)
+    run_cont("restore_window", sl, True, True, odd=False)
