@@ -213,6 +213,16 @@ int lzckpt_engine_wait_persisted(lzckpt_engine* e, lzckpt_ticket* k);
 int lzckpt_engine_drain(lzckpt_engine* e);
 int lzckpt_engine_restore(lzckpt_engine* e, const lzckpt_manifest* m, uint64_t step, lzckpt_tree** out);
 int lzckpt_engine_restore_into(lzckpt_engine* e, const lzckpt_manifest* m, uint64_t step, lzckpt_tree* t);
+/* Two-phase commit of a persisted capture (CommitCoordinator::run_step with
+ * this engine as the participant; reference consolidation.cpp:160-284): the
+ * files are validated (header, extent, entry checksums) and their whole-file
+ * digests recorded in the manifest, each file read once and hashed on the
+ * GPU. Single-rank topologies. *committed = 1 when the step committed, else
+ * `reason` says why. */
+int lzckpt_engine_commit(lzckpt_engine* e, const lzckpt_model_spec* model, lzckpt_ticket* t, lzckpt_manifest* m,
+                         int* committed, char* reason, uint64_t reason_cap);
+/* FNV-1a-64 and length of a whole file (the manifest digest), on the GPU. */
+int lzckpt_file_digest(const char* path, int device, uint64_t* length, uint64_t* digest);
 
 typedef struct lzckpt_counters {
   uint64_t captures;

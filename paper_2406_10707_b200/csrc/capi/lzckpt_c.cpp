@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 
+#include "lzckpt/consolidation.hpp"
 #include "lzckpt/engine.hpp"
 #include "lzckpt/errors.hpp"
 #include "lzckpt/format.hpp"
@@ -17,6 +18,7 @@
 #include "lzckpt/topology.hpp"
 #include "lzckpt/workload.hpp"
 #include "lzk_cuda.h"
+#include "../src/file_stream.hpp"
 
 using namespace lzckpt;
 
@@ -572,6 +574,40 @@ int lzckpt_engine_restore_into(lzckpt_engine* e, const lzckpt_manifest* m, uint6
     need(m, "manifest");
     need(t, "tree");
     e->e->restore_into(*m->m, step, t->t);
+  });
+}
+
+int lzckpt_file_digest(const char* path, int device, uint64_t* length, uint64_t* digest) {
+  return guard([&] {
+    need(path, "path");
+    need(length, "length");
+    need(digest, "digest");
+    detail::FileStreamer streamer(device);
+    *digest = streamer.digest(path, length);
+  });
+}
+
+int lzckpt_engine_commit(lzckpt_engine* e, const lzckpt_model_spec* model, lzckpt_ticket* t, lzckpt_manifest* m,
+                         int* committed, char* reason, uint64_t reason_cap) {
+  return guard([&] {
+    need(e, "engine");
+    need(model, "model");
+    need(t, "ticket");
+    need(m, "manifest");
+    need(committed, "committed");
+    if (e->topo.ranks() != 1) {
+      throw ConfigError("lzckpt_engine_commit: single-rank topologies only (one participant per process)");
+    }
+    const uint64_t step = t->k->step();
+    const CheckpointPlan plan = plan_checkpoint(e->topo, to_model(model), step);
+    EngineCommitParticipant part(*e->e, plan, t->k);
+    CommitCoordinator coord(*m->m, e->topo);
+    const CommitRecord rec = coord.run_step(step, {&part});
+    *committed = rec.decision == Decision::Committed ? 1 : 0;
+    if (reason && reason_cap) {
+      std::strncpy(reason, rec.reason.c_str(), size_t(reason_cap) - 1);
+      reason[reason_cap - 1] = '\0';
+    }
   });
 }
 

@@ -27,38 +27,19 @@
 #include <thread>
 #include <utility>
 
+#include "file_stream.hpp"
 #include "lzckpt/errors.hpp"
 #include "lzk_cuda.h"
 
 namespace lzckpt {
 
+using detail::ck;
+using detail::EntrySink;
+using detail::FileStreamer;
+using detail::PhaseTrace;
+using detail::since;
+
 namespace {
-
-void ck(int rc, const char* what) {
-  if (rc != LZK_OK) throw DeviceError(std::string(what) + ": " + lzk_last_error());
-}
-
-double since(std::chrono::steady_clock::time_point t0) {
-  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-}
-
-// LZCKPT_TRACE=1: per-phase capture timing on stderr (host-overhead tuning).
-struct PhaseTrace {
-  explicit PhaseTrace(const char* what = "capture") : what(what) {}
-  const char* what;
-  bool on = std::getenv("LZCKPT_TRACE") != nullptr;
-  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
-  std::string line;
-  void mark(const char* name) {
-    if (!on) return;
-    const auto now = std::chrono::steady_clock::now();
-    line += std::string(" ") + name + "=" + std::to_string(std::chrono::duration<double, std::milli>(now - t).count());
-    t = now;
-  }
-  ~PhaseTrace() {
-    if (on) std::fprintf(stderr, "[lzckpt %s ms]%s\n", what, line.c_str());
-  }
-};
 
 struct ShardBuild {
   uint64_t shard_id = 0;
@@ -91,47 +72,6 @@ struct Pinned {
     cap = n;
   }
 };
-
-// Runs fn(i) for i in [0, n) on up to `threads` threads.
-template <class Fn>
-void parallel_for(size_t n, unsigned threads, Fn fn) {
-  if (n == 0) return;
-  threads = unsigned(std::min<size_t>(threads, n));
-  if (threads <= 1) {
-    for (size_t i = 0; i < n; ++i) fn(i);
-    return;
-  }
-  std::atomic<size_t> next{0};
-  std::vector<std::thread> th;
-  std::exception_ptr err;
-  std::mutex err_mu;
-  for (unsigned t = 0; t < threads; ++t) {
-    th.emplace_back([&] {
-      for (size_t i; (i = next.fetch_add(1)) < n;) {
-        try {
-          fn(i);
-        } catch (...) {
-          std::lock_guard lk(err_mu);
-          if (!err) err = std::current_exception();
-        }
-      }
-    });
-  }
-  for (auto& x : th) x.join();
-  if (err) std::rethrow_exception(err);
-}
-
-void pread_all(int fd, void* dst, uint64_t n, uint64_t off, const std::filesystem::path& p) {
-  auto* d = static_cast<char*>(dst);
-  while (n) {
-    ssize_t r = ::pread(fd, d, n, off_t(off));
-    if (r < 0 && errno == EINTR) continue;
-    if (r <= 0) throw IoError("read failed for " + p.string());
-    d += r;
-    off += uint64_t(r);
-    n -= uint64_t(r);
-  }
-}
 
 }  // namespace
 
@@ -703,179 +643,6 @@ std::vector<std::byte> read_entry(const std::filesystem::path& file, const Check
 
 namespace {
 
-// Where one entry's bytes go during restore.
-struct EntrySink {
-  void* device = nullptr;                 // region memory (DMA target), or
-  std::vector<std::byte>* host = nullptr; // a host buffer (blobs, __meta__)
-};
-
-// Streams one committed shard file through a few pinned windows. A reader
-// thread preads window i+1 while window i goes to HBM in one DMA; there its
-// entry slices are checksummed on the GPU (lzk_fnv1a64_continue: per-entry
-// FNV-1a states continued across windows, kept in mapped host memory) and
-// scattered device-to-device into their device sinks; host sinks are copied
-// from the pinned window. No byte is hashed on the host. Memory stays bounded
-// by the windows whatever the file size (C2's optimizer file is 84 GB).
-// Returns the keys whose checksum mismatches (the caller decides what that
-// voids).
-class FileStreamer {
- public:
-  static constexpr uint64_t kWindow = 512ull << 20;
-  static constexpr int kWindows = 3;
-
-  FileStreamer(int device, uint64_t /*ce_threshold*/) : device_(device) {
-    ck(lzk_stream_create(device, 0, &stream_), "restore stream");
-    for (auto& w : win_) ck(lzk_event_create(device, 1, &w.done), "restore event");
-  }
-  ~FileStreamer() {
-    for (auto& w : win_) {
-      if (w.done) lzk_event_destroy(w.done);
-      lzk_host_free(w.buf);
-      lzk_dev_free(device_, w.dbuf);
-    }
-    lzk_host_free(states_);
-    lzk_stream_destroy(stream_);
-  }
-
-  std::vector<std::string> run(const std::filesystem::path& path, const CheckpointFileHeader& h,
-                               const std::vector<EntrySink>& sinks) {
-    PhaseTrace tr("restore_stream");
-    const uint64_t hsize = h.serialized_size(), end = h.payload_end();
-    const int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
-    if (fd < 0) throw IoError("cannot open " + path.string());
-    struct Closer {
-      int fd;
-      ~Closer() { ::close(fd); }
-    } closer{fd};
-    const uint64_t n = end - hsize;
-    const uint64_t wsize = std::min(kWindow, std::max<uint64_t>(n, 1));
-    const size_t slots = size_t(std::min<uint64_t>(kWindows, (n + wsize - 1) / wsize));
-    for (size_t k = 0; k < size_t(kWindows); ++k) {
-      Window& w = win_[k];
-      if (k < slots && w.cap < wsize) {
-        lzk_host_free(w.buf);
-        w.buf = nullptr;
-        lzk_dev_free(device_, w.dbuf);
-        w.dbuf = nullptr;
-        void* p = nullptr;
-        ck(lzk_host_alloc(wsize, LZK_HOST_MAPPED | LZK_HOST_HUGEPAGE, &p), "restore window");
-        w.buf = static_cast<std::byte*>(p);
-        tr.mark("host_window");
-        ck(lzk_dev_alloc(device_, wsize, &p), "restore device window");
-        w.dbuf = static_cast<std::byte*>(p);
-        tr.mark("dev_window");
-        w.cap = wsize;
-      }
-      w.used = false;
-    }
-    // per-entry running digests, written by the GPU
-    const size_t ne = h.entries.size();
-    if (states_cap_ < ne) {
-      lzk_host_free(states_);
-      void* p = nullptr;
-      ck(lzk_host_alloc(std::max<size_t>(ne, 1) * 8, LZK_HOST_MAPPED, &p), "restore digests");
-      states_ = static_cast<uint64_t*>(p);
-      states_cap_ = ne;
-    }
-    for (size_t e = 0; e < ne; ++e) states_[e] = Fnv64::kOffset;
-    tr.mark("setup");
-    double wait_read = 0, t_h2d = 0, t_hash = 0, t_d2d = 0;
-    const size_t nwin = size_t((n + wsize - 1) / wsize);
-    // reader: window i -> slot i % kWindows (waits until the slot's DMA finished)
-    auto read_window = [&](size_t i) {
-      Window& w = win_[i % kWindows];
-      if (w.used) ck(lzk_event_sync(w.done), "restore window reuse");
-      const uint64_t off = uint64_t(i) * wsize, len = std::min(wsize, n - off);
-      const uint64_t piece = 64ull << 20;
-      parallel_for(size_t((len + piece - 1) / piece), 8, [&](size_t k) {
-        const uint64_t o = uint64_t(k) * piece;
-        pread_all(fd, w.buf + o, std::min(piece, len - o), hsize + off + o, path);
-      });
-    };
-    std::thread reader;
-    std::exception_ptr read_err;
-    if (nwin) read_window(0);
-    tr.mark("read0");
-    for (size_t i = 0; i < nwin; ++i) {
-      const auto tw = std::chrono::steady_clock::now();
-      if (reader.joinable()) reader.join();
-      wait_read += since(tw);
-      if (read_err) std::rethrow_exception(read_err);
-      Window& w = win_[i % kWindows];
-      const uint64_t off = uint64_t(i) * wsize, len = std::min(wsize, n - off);
-      lzk_copy_desc up{reinterpret_cast<uint64_t>(w.buf), reinterpret_cast<uint64_t>(w.dbuf), len};
-      ck(lzk_ce_copy_h2d(stream_, &up, 1), "restore DMA");
-      ck(lzk_event_record(w.done, stream_), "restore event");  // host window reusable after this
-      w.used = true;
-      if (i + 1 < nwin) {
-        reader = std::thread([&, i] {
-          try {
-            read_window(i + 1);
-          } catch (...) {
-            read_err = std::current_exception();
-          }
-        });
-      }
-      // entry slices overlapping [off, off + len) of the payload
-      std::vector<lzk_hash_desc> hd;
-      std::vector<lzk_copy_desc> d2d;
-      for (size_t e = 0; e < ne; ++e) {
-        const uint64_t eb = h.entries[e].offset - hsize, ee = eb + h.entries[e].length;
-        const uint64_t a = std::max(eb, off), b = std::min(ee, off + len);
-        if (a >= b) continue;
-        const uint64_t src = reinterpret_cast<uint64_t>(w.dbuf + (a - off));
-        hd.push_back({src, b - a, 0, reinterpret_cast<uint64_t>(states_ + e)});
-        const EntrySink& s = sinks[e];
-        if (s.device) {
-          d2d.push_back({src, reinterpret_cast<uint64_t>(static_cast<std::byte*>(s.device) + (a - eb)), b - a});
-        } else if (s.host) {
-          std::memcpy(s.host->data() + (a - eb), w.buf + (a - off), b - a);
-        }
-      }
-      auto gpu_mark = [&](double& acc) {  // trace only: serializes the pipeline
-        if (!tr.on) return;
-        const auto t0 = std::chrono::steady_clock::now();
-        ck(lzk_stream_sync(stream_), "restore trace sync");
-        acc += since(t0);
-      };
-      gpu_mark(t_h2d);
-      if (!hd.empty()) ck(lzk_fnv1a64_continue(stream_, hd.data(), uint32_t(hd.size()), 0), "restore checksums");
-      gpu_mark(t_hash);
-      if (!d2d.empty()) ck(lzk_gather_d2d(stream_, d2d.data(), uint32_t(d2d.size()), 0), "restore scatter");
-      gpu_mark(t_d2d);
-    }
-    if (reader.joinable()) reader.join();
-    if (read_err) std::rethrow_exception(read_err);
-    tr.mark("windows");
-    ck(lzk_stream_sync(stream_), "restore sync");
-    tr.mark("sync");
-    if (tr.on) {
-      tr.line += " read_wait=" + std::to_string(wait_read * 1e3) + " h2d=" + std::to_string(t_h2d * 1e3) +
-                 " hash=" + std::to_string(t_hash * 1e3) + " d2d=" + std::to_string(t_d2d * 1e3) +
-                 " nwin=" + std::to_string(nwin);
-    }
-    std::vector<std::string> bad;
-    for (size_t e = 0; e < ne; ++e) {
-      if (states_[e] != h.entries[e].checksum) bad.push_back(h.entries[e].key);
-    }
-    return bad;
-  }
-
- private:
-  struct Window {
-    std::byte* buf = nullptr;   // pinned host
-    std::byte* dbuf = nullptr;  // device copy of the window
-    uint64_t cap = 0;
-    lzk_event* done = nullptr;
-    bool used = false;
-  };
-  int device_;
-  lzk_stream* stream_ = nullptr;
-  Window win_[kWindows];
-  uint64_t* states_ = nullptr;
-  size_t states_cap_ = 0;
-};
-
 // Header + exact-extent check (reference read_header + validate_entries
 // length rule, format.cpp:173-214) and the parsed __meta__ leaf manifest.
 std::vector<LeafManifestEntry> open_shard(const std::filesystem::path& path, CheckpointFileHeader& h) {
@@ -1025,7 +792,7 @@ void restore_one(const std::filesystem::path& path, StateTree& tree, const State
 StateTree Engine::restore(const ManifestStore& manifest, uint64_t step) const {
   const auto files = manifest.files_for(step);  // NotCommitted
   const std::string prefix = step_dirname(step) + "/" + rank_dirname(rank_) + "/";
-  FileStreamer streamer(transfers_.device(), config_.snapshot.ce_threshold);
+  FileStreamer streamer(transfers_.device());
   StateTree tree;
   for (const auto& rec : files) {
     if (rec.relative_path.rfind(prefix, 0) != 0) continue;
@@ -1035,7 +802,7 @@ StateTree Engine::restore(const ManifestStore& manifest, uint64_t step) const {
 }
 
 StateTree Engine::restore_file(const std::filesystem::path& path, const StateTree* into) const {
-  FileStreamer streamer(transfers_.device(), config_.snapshot.ce_threshold);
+  FileStreamer streamer(transfers_.device());
   StateTree tree;
   restore_one(path, tree, into, transfers_.device(), streamer);
   return tree;
@@ -1045,7 +812,7 @@ void Engine::restore_into(const ManifestStore& manifest, uint64_t step, StateTre
   const auto files = manifest.files_for(step);
   const std::string prefix = step_dirname(step) + "/" + rank_dirname(rank_) + "/";
   const int dev = transfers_.device();
-  FileStreamer streamer(dev, config_.snapshot.ce_threshold);
+  FileStreamer streamer(dev);
   struct Plan {
     std::filesystem::path path;
     CheckpointFileHeader h;

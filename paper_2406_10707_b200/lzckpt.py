@@ -685,6 +685,16 @@ class Engine:
     def restore_into(self, manifest: ManifestStore, step: int, tree: StateTree) -> None:
         _check(lib.lzckpt_engine_restore_into(self._h, manifest._h, step, tree._h))
 
+    def commit(self, model: ModelSpec, t: CaptureTicket, manifest: ManifestStore) -> Tuple[bool, str]:
+        """Two-phase commit of a persisted capture (reference
+        CommitCoordinator::run_step, consolidation.cpp:160-284): files are
+        validated and their whole-file digests recorded, each file read once
+        and hashed on the GPU. Returns (committed, reason)."""
+        ok = C.c_int()
+        reason = C.create_string_buffer(1024)
+        _check(lib.lzckpt_engine_commit(self._h, C.byref(model._c()), t._h, manifest._h, C.byref(ok), reason, 1024))
+        return bool(ok.value), reason.value.decode(errors="replace")
+
     def counters(self) -> Counters:
         c = N.CountersC()
         _check(lib.lzckpt_engine_counters(self._h, C.byref(c)))
@@ -714,15 +724,20 @@ class Engine:
         return lib.lzckpt_engine_snapshot_stream(self._h) or 0
 
 
-def committed_record(ticket: CaptureTicket, root: str, digest: bool = False) -> List[Tuple[str, int, int]]:
-    """Manifest rows for a persisted ticket (reference test_engine.cpp:73-84)."""
+def committed_record(ticket: CaptureTicket, root: str, digest: bool = False,
+                     device: int = 0) -> List[Tuple[str, int, int]]:
+    """Manifest rows for a persisted ticket (reference test_engine.cpp:73-84);
+    with digest=True the whole-file FNV-1a the manifest records, computed on
+    the GPU (lzckpt_file_digest)."""
     rows = []
     for f in ticket.shard_files():
         d = 0
+        n = os.path.getsize(f)
         if digest:
-            with open(f, "rb") as fh:
-                d = fnv64(fh.read())
-        rows.append((os.path.relpath(f, root), os.path.getsize(f), d))
+            ln, dg = C.c_uint64(), C.c_uint64()
+            _check(lib.lzckpt_file_digest(os.fspath(f).encode(), device, C.byref(ln), C.byref(dg)))
+            n, d = ln.value, dg.value
+        rows.append((os.path.relpath(f, root), n, d))
     return rows
 
 
