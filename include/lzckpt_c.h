@@ -221,6 +221,9 @@ int lzckpt_engine_restore_into(lzckpt_engine* e, const lzckpt_manifest* m, uint6
  * `reason` says why. */
 int lzckpt_engine_commit(lzckpt_engine* e, const lzckpt_model_spec* model, lzckpt_ticket* t, lzckpt_manifest* m,
                          int* committed, char* reason, uint64_t reason_cap);
+/* Restore/commit keep their pinned + device stream windows (3 x 512 MiB each)
+ * pooled for the next call; this frees the idle ones. */
+void lzckpt_trim_caches(void);
 /* FNV-1a-64 and length of a whole file (the manifest digest), on the GPU. */
 int lzckpt_file_digest(const char* path, int device, uint64_t* length, uint64_t* digest);
 

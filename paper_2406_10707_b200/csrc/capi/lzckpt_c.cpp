@@ -582,10 +582,12 @@ int lzckpt_file_digest(const char* path, int device, uint64_t* length, uint64_t*
     need(path, "path");
     need(length, "length");
     need(digest, "digest");
-    detail::FileStreamer streamer(device);
-    *digest = streamer.digest(path, length);
+    auto streamer = detail::FileStreamer::acquire(device);
+    *digest = streamer->digest(path, length);
   });
 }
+
+void lzckpt_trim_caches(void) { detail::FileStreamer::trim(); }
 
 int lzckpt_engine_commit(lzckpt_engine* e, const lzckpt_model_spec* model, lzckpt_ticket* t, lzckpt_manifest* m,
                          int* committed, char* reason, uint64_t reason_cap) {

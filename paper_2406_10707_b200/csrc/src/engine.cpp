@@ -792,19 +792,19 @@ void restore_one(const std::filesystem::path& path, StateTree& tree, const State
 StateTree Engine::restore(const ManifestStore& manifest, uint64_t step) const {
   const auto files = manifest.files_for(step);  // NotCommitted
   const std::string prefix = step_dirname(step) + "/" + rank_dirname(rank_) + "/";
-  FileStreamer streamer(transfers_.device());
+  auto streamer = FileStreamer::acquire(transfers_.device());
   StateTree tree;
   for (const auto& rec : files) {
     if (rec.relative_path.rfind(prefix, 0) != 0) continue;
-    restore_one(config_.checkpoint_root / rec.relative_path, tree, nullptr, transfers_.device(), streamer);
+    restore_one(config_.checkpoint_root / rec.relative_path, tree, nullptr, transfers_.device(), *streamer);
   }
   return tree;
 }
 
 StateTree Engine::restore_file(const std::filesystem::path& path, const StateTree* into) const {
-  FileStreamer streamer(transfers_.device());
+  auto streamer = FileStreamer::acquire(transfers_.device());
   StateTree tree;
-  restore_one(path, tree, into, transfers_.device(), streamer);
+  restore_one(path, tree, into, transfers_.device(), *streamer);
   return tree;
 }
 
@@ -812,7 +812,7 @@ void Engine::restore_into(const ManifestStore& manifest, uint64_t step, StateTre
   const auto files = manifest.files_for(step);
   const std::string prefix = step_dirname(step) + "/" + rank_dirname(rank_) + "/";
   const int dev = transfers_.device();
-  FileStreamer streamer(dev);
+  auto streamer = FileStreamer::acquire(dev);
   struct Plan {
     std::filesystem::path path;
     CheckpointFileHeader h;
@@ -833,7 +833,7 @@ void Engine::restore_into(const ManifestStore& manifest, uint64_t step, StateTre
       }
       if (!l.inlined && !p.h.find(l.path)) throw FormatError(p.path.string() + ": no entry named '" + l.path + "'");
     }
-    throw_bad(p.path, streamer.run(p.path, p.h, std::vector<EntrySink>(p.h.entries.size())));
+    throw_bad(p.path, streamer->run(p.path, p.h, std::vector<EntrySink>(p.h.entries.size())));
     plans.push_back(std::move(p));
   }
   // pass 2: DMA into the live regions (blobs are host state, left to restore())
@@ -861,7 +861,7 @@ void Engine::restore_into(const ManifestStore& manifest, uint64_t step, StateTre
       }
       touched.push_back(std::move(r));
     }
-    throw_bad(p.path, streamer.run(p.path, p.h, sinks));
+    throw_bad(p.path, streamer->run(p.path, p.h, sinks));
     if (!inl.empty()) {
       lzk_stream* s = nullptr;
       ck(lzk_stream_create(dev, 0, &s), "restore stream");

@@ -88,6 +88,44 @@ FileStreamer::~FileStreamer() {
   lzk_stream_destroy(stream_);
 }
 
+namespace {
+std::mutex g_pool_mu;
+std::vector<FileStreamer*> g_pool;  // idle streamers (any device)
+constexpr size_t kPoolMax = 4;
+}  // namespace
+
+FileStreamer::Handle FileStreamer::acquire(int device) {
+  {
+    std::lock_guard lk(g_pool_mu);
+    for (size_t i = 0; i < g_pool.size(); ++i) {
+      if (g_pool[i]->device_ == device) {
+        FileStreamer* s = g_pool[i];
+        g_pool.erase(g_pool.begin() + long(i));
+        return Handle(s);
+      }
+    }
+  }
+  return Handle(new FileStreamer(device));
+}
+
+void FileStreamer::Release::operator()(FileStreamer* s) const {
+  std::lock_guard lk(g_pool_mu);
+  if (g_pool.size() < kPoolMax) {
+    g_pool.push_back(s);
+    return;
+  }
+  delete s;
+}
+
+void FileStreamer::trim() {
+  std::vector<FileStreamer*> idle;
+  {
+    std::lock_guard lk(g_pool_mu);
+    idle.swap(g_pool);
+  }
+  for (auto* s : idle) delete s;
+}
+
 void FileStreamer::ensure_states(size_t n) {
   if (states_cap_ >= n) return;
   lzk_host_free(states_);

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <filesystem>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -71,6 +72,17 @@ class FileStreamer {
                                const std::vector<EntrySink>& sinks, uint64_t* file_digest = nullptr);
   // FNV-1a-64 and length of any whole file (no header needed).
   uint64_t digest(const std::filesystem::path& path, uint64_t* length);
+
+  // Streamers are pooled per device: pinned and device windows stay
+  // allocated between restores and commits (first-use allocation of the
+  // windows costs hundreds of ms). The handle returns it to the pool.
+  struct Release {
+    void operator()(FileStreamer* s) const;
+  };
+  using Handle = std::unique_ptr<FileStreamer, Release>;
+  static Handle acquire(int device);
+  // Frees the idle pooled streamers (their pinned and device windows).
+  static void trim();
 
  private:
   struct Window {

@@ -363,6 +363,13 @@ void FlushPipeline::run_write(FileRecord& f, const Job& j, const std::byte* src)
     std::this_thread::sleep_until(until);
   }
   pwrite_all(f.fd, src, j.length, f.header_size + j.offset, f.path);
+  // Durable files: start writeback of this piece now. The kernel's own
+  // background writeback only begins past dirty_background_ratio (~19 GB on
+  // the B200 hosts), so without this a whole checkpoint is written back
+  // inside the final fsync, after the pipeline has finished.
+  if (config_.fsync_on_finalize) {
+    ::sync_file_range(f.fd, off_t(f.header_size + j.offset), off_t(j.length), SYNC_FILE_RANGE_WRITE);
+  }
 }
 
 // Hands the file's resident-but-unwritten bytes to the writers: full pieces
