@@ -224,6 +224,14 @@ int lzckpt_engine_commit(lzckpt_engine* e, const lzckpt_model_spec* model, lzckp
 /* Restore/commit keep their pinned + device stream windows (3 x 512 MiB each)
  * pooled for the next call; this frees the idle ones. */
 void lzckpt_trim_caches(void);
+/* Phase one of the 2PC for THIS rank only (EngineCommitParticipant::prepare,
+ * reference consolidation.cpp:142-152): waits until the capture is persisted,
+ * then validates the rank's files on the GPU. Writes a JSON vote
+ * {"rank","step","vote":"prepared"|"failed","detail","files":[[path,length,digest]]}
+ * into `json` when `cap` >= *needed (always set). Multi-process jobs gather
+ * these votes over their own transport (paper_2406_10707_b200/commit.py). */
+int lzckpt_engine_prepare(lzckpt_engine* e, const lzckpt_model_spec* model, lzckpt_ticket* t, char* json,
+                          uint64_t cap, uint64_t* needed);
 /* FNV-1a-64 and length of a whole file (the manifest digest), on the GPU. */
 int lzckpt_file_digest(const char* path, int device, uint64_t* length, uint64_t* digest);
 

@@ -149,6 +149,7 @@ ENGINE_SYMBOLS = [
     ("lzckpt_engine_commit", i32, [vp, P(ModelSpecC), vp, vp, P(i32), cp, u64]),
     ("lzckpt_file_digest", i32, [cp, i32, P(u64), P(u64)]),
     ("lzckpt_trim_caches", None, []),
+    ("lzckpt_engine_prepare", i32, [vp, P(ModelSpecC), vp, cp, u64, P(u64)]),
     ("lzckpt_engine_ticket_header", i32, [vp, vp, u32, P(vp)]),
     ("lzckpt_engine_restore_file", i32, [vp, cp, vp, P(vp)]),
     ("lzckpt_ticket_release", None, [vp]),

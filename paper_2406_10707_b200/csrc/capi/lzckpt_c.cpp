@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "lzckpt/consolidation.hpp"
+#include <json.hpp>
 #include "lzckpt/engine.hpp"
 #include "lzckpt/errors.hpp"
 #include "lzckpt/format.hpp"
@@ -588,6 +589,32 @@ int lzckpt_file_digest(const char* path, int device, uint64_t* length, uint64_t*
 }
 
 void lzckpt_trim_caches(void) { detail::FileStreamer::trim(); }
+
+int lzckpt_engine_prepare(lzckpt_engine* e, const lzckpt_model_spec* model, lzckpt_ticket* t, char* json,
+                          uint64_t cap, uint64_t* needed) {
+  return guard([&] {
+    need(e, "engine");
+    need(model, "model");
+    need(t, "ticket");
+    need(needed, "needed");
+    const uint64_t step = t->k->step();
+    const CheckpointPlan plan = plan_checkpoint(e->topo, to_model(model), step);
+    EngineCommitParticipant part(*e->e, plan, t->k);
+    const auto rep = part.prepare(step);  // wait_persisted + GPU validation of this rank's files
+    nlohmann::json j;
+    j["rank"] = part.flat_rank();
+    j["step"] = step;
+    j["vote"] = rep && rep->vote == Vote::Prepared ? "prepared" : "failed";
+    j["detail"] = rep ? rep->detail : "no answer";
+    j["files"] = nlohmann::json::array();
+    if (rep) {
+      for (const auto& f : rep->files) j["files"].push_back({f.relative_path, f.length, f.digest});
+    }
+    const std::string out = j.dump();
+    *needed = out.size() + 1;
+    if (json && cap >= out.size() + 1) std::memcpy(json, out.c_str(), out.size() + 1);
+  });
+}
 
 int lzckpt_engine_commit(lzckpt_engine* e, const lzckpt_model_spec* model, lzckpt_ticket* t, lzckpt_manifest* m,
                          int* committed, char* reason, uint64_t reason_cap) {

@@ -76,3 +76,20 @@ def test_commit_rejects_corrupt_and_truncated(gpu, tmp_path):
     assert not ok and why, why
     assert not m.is_committed(6)
     eng.close()
+
+
+def test_prepare_vote_and_distributed_commit(gpu, oracle, tmp_path):
+    """lzckpt_engine_prepare (this rank's GPU-validated vote) feeding
+    commit.distributed_commit (world of one process here; the gloo protocol
+    test covers N=2)."""
+    from paper_2406_10707_b200.commit import distributed_commit, prepare
+    eng, t = persisted(gpu, tmp_path)
+    v = prepare(eng, tiny_model(gpu), t)
+    assert v["vote"] == "prepared" and v["rank"] == 0 and v["step"] == 5, v
+    got = {p: (n, d) for p, n, d in v["files"]}
+    for f in t.shard_files():
+        assert got[os.path.relpath(f, tmp_path)] == (os.path.getsize(f), file_fnv(oracle, f))
+    rec = distributed_commit(eng, tiny_model(gpu), t, str(tmp_path / "manifest.json"))
+    assert rec.committed and rec.step == 5
+    assert gpu.ManifestStore(str(tmp_path / "manifest.json")).is_committed(5)
+    eng.close()

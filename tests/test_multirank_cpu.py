@@ -63,3 +63,54 @@ def test_two_rank_plans_are_disjoint_and_complete():
     assert len(all_files) == len(set(all_files)) == 2 * world
     assert sum(b for _, b in gathered) == total
     assert tmax == 2.0
+
+
+def _commit_worker(rank, world, port, root, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2406_10707_b200.commit import distributed_commit
+    manifest = os.path.join(root, "manifest.json")
+
+    def vote(step, ok):
+        files = [[f"step-{step}/rank-{rank}-0-0/layers-{rank}-{rank}.ckpt", 100 + rank, 0xA0 + rank],
+                 [f"step-{step}/rank-{rank}-0-0/optimizer-{rank}.ckpt", 200 + rank, 0xB0 + rank]]
+        return {"rank": rank, "step": step, "vote": "prepared" if ok else "failed",
+                "detail": "" if ok else "checksum mismatch in entry 'w'", "files": files if ok else []}
+
+    r1 = distributed_commit(None, None, None, manifest, prepare_fn=lambda: vote(3, True))
+    r2 = distributed_commit(None, None, None, manifest, prepare_fn=lambda: vote(4, rank == 0))
+    out.put((rank, r1, r2))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_distributed_commit(tmp_path):
+    """paper_2406_10707_b200/commit.py over gloo: votes gathered to rank 0,
+    the reference coordinator's decision (consolidation.cpp:229-283), the
+    manifest made durable by rank 0 before the decision is broadcast; an
+    aborted step blames the failing rank and leaves the manifest untouched."""
+    import json
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_commit_worker, args=(r, world, port, str(tmp_path), q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        rank, r1, r2 = q.get(timeout=240)
+        res[rank] = (r1, r2)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank in range(world):
+        r1, r2 = res[rank]
+        assert r1.committed and r1.step == 3
+        assert not r2.committed and r2.problem_ranks == [1]
+        assert r2.reason == "rank 1: checksum mismatch in entry 'w'"
+    m = json.load(open(tmp_path / "manifest.json"))
+    assert [s["step"] for s in m["steps"]] == [3]
+    paths = [f["path"] for f in m["steps"][0]["files"]]
+    assert paths == sorted(paths) and len(paths) == 4
+    assert {f["length"] for f in m["steps"][0]["files"]} == {100, 101, 200, 201}
