@@ -318,7 +318,7 @@ def main_ours(args, rank, world, local_rank):
             eng.close()
             del eng
             try:
-                e2e = e2e_persisted(lz, torch, dev, tmp, args, world)
+                e2e = e2e_persisted(lz, torch, dev, tmp, args, world, rank)
                 # whole-job figure: bytes of all ranks over the slowest rank's time
                 t_max = max_over_ranks(e2e.pop("seconds"))
                 e2e["per_rank_gbps"] = e2e["value"]
@@ -517,25 +517,36 @@ def train_loop(lz, torch, eng, plan, built, payload, gbps, barrier):
             "fence": "update_barrier_on_stream (device-side)", "gemm": "bf16 8192^3 torch.matmul x%d" % n_mm}
 
 
-def e2e_persisted(lz, torch, dev, tmp, args, world=1):
+def e2e_persisted(lz, torch, dev, tmp, args, world=1, rank=0):
     """Public API end to end with durable files: capture -> update_barrier ->
     wait_persisted (pwrite + per-entry FNV + header last + fsync) on a
-    bounded C2 slice that fits the box's local disk (all ranks write to it:
-    2 decoder layers + embeddings at N<=2, 1 layer at N>2)."""
+    bounded C2 slice that fits the box's local disk: a dp=N plan where each
+    rank owns a 2-decoder-layer shard at N<=2, 1 at N>2 (weak scaling), every
+    rank writing its shards under ONE shared root. The last step is committed
+    by the two-phase commit (N>1: commit.distributed_commit over
+    torch.distributed) and restored."""
     from paper_2406_10707_b200.workloads import llama7b_shard
-    layers = 2 if world <= 2 else 1
-    w = llama7b_shard(layers=layers, vocab=8000, name=f"c2-slice-{layers}l")
+    per_rank = 2 if world <= 2 else 1
+    w = llama7b_shard(layers=per_rank, vocab=8000, dp=world, rank=rank, name=f"c2-slice-{per_rank}l-dp{world}")
     spec = w.write_spec(os.path.join(tmp, "e2e.spec"))
     built = lz.build_workload(spec, dev)
-    root = os.path.join(tmp, "e2e_ckpt")
+    root = os.path.join(ROOT, f"lzk_e2e_{os.environ.get('MASTER_PORT', 'solo')}") if world > 1 \
+        else os.path.join(tmp, "e2e_ckpt")
+
+    def sync():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+
     cfg = lz.EngineConfig(checkpoint_root=root, host_buffer_bytes=int(built.bytes * 1.01) + (64 << 20),
                           fsync_on_finalize=True, device=dev)
     eng = lz.Engine(cfg, built.topo, built.rank)
     plan = lz.plan_checkpoint(built.topo, built.model, built.step)
     times = []
     steps = 3
+    r0, r1, r2 = built.rank.dp, built.rank.pp, built.rank.tp
     for s in range(steps):
-        torch.cuda.synchronize()
+        sync()
         h0 = time.perf_counter()
         t = eng.capture(plan, built.tree, 700 + s)
         eng.update_barrier(t)
@@ -544,15 +555,22 @@ def e2e_persisted(lz, torch, dev, tmp, args, world=1):
         if s >= 1:
             times.append(dt)
         payload = t.payload_bytes()
-        if s + 1 < steps:
-            shutil.rmtree(os.path.join(root, f"step-{700 + s}"), ignore_errors=True)
+        if s + 1 < steps:  # each rank removes only its own directory
+            shutil.rmtree(os.path.join(root, f"step-{700 + s}", f"rank-{r0}-{r1}-{r2}"), ignore_errors=True)
     # two-phase commit of the last step: files validated and digested on the GPU
-    m = lz.ManifestStore(os.path.join(root, "manifest.json"))
+    mpath = os.path.join(root, "manifest.json")
+    sync()
     h0 = time.perf_counter()
-    committed, why = eng.commit(built.model, t, m)
+    if world > 1:
+        from paper_2406_10707_b200.commit import distributed_commit
+        rec = distributed_commit(eng, built.model, t, mpath)
+        committed, why = rec.committed, rec.reason
+    else:
+        committed, why = eng.commit(built.model, t, lz.ManifestStore(mpath))
     commit_s = time.perf_counter() - h0
     if not committed:
         raise RuntimeError("commit failed: " + why)
+    m = lz.ManifestStore(mpath)
     # restore the last step (files just written: page cache may be warm)
     h0 = time.perf_counter()
     back = eng.restore(m, 700 + steps - 1)
@@ -562,13 +580,17 @@ def e2e_persisted(lz, torch, dev, tmp, args, world=1):
     ok = ok and all(back.region_at(l.path).clone_bytes() == built.tree.region_at(l.path).clone_bytes() for l in probe)
     del back
     eng.close()
+    sync()
+    if world > 1 and rank == 0:
+        shutil.rmtree(root, ignore_errors=True)
     v = payload * len(times) / sum(times) / 1e9
     return {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": payload,
             "seconds": sum(times),
             "workload": f"{w.name} ({payload} B payload per rank, {len(w.leaves)} tensors)",
             "path": "capture -> update_barrier -> wait_persisted, fsync, local disk", "steps": len(times),
             "commit_gbps": round(payload / commit_s / 1e9, 3),
-            "commit_path": "2PC CommitCoordinator: each file read once, entry checksums + whole-file digest on the GPU",
+            "commit_seconds": round(commit_s, 3),
+            "commit_path": "2PC (N>1: votes over torch.distributed): each file read once, entry checksums + whole-file digest on the GPU",
             "restore_gbps": round(payload / restore_s / 1e9, 3), "restore_spot_check": ok,
             "restore_path": "parallel pread into pinned windows -> one DMA per window -> device FNV check -> D2D to regions"}
 
