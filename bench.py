@@ -480,9 +480,12 @@ def train_loop(lz, torch, eng, plan, built, payload, gbps, barrier):
         with torch.cuda.stream(comp):
             for _ in range(n_mm):
                 torch.matmul(a, b, out=c)  # forward + backward stand-in
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if ckpt:
             if device_fence:
+                f0.record(comp)  # compute stream reaches the fence
                 eng.update_barrier_on_stream(t, comp.cuda_stream)
+                f1.record(comp)  # ... and passes it
             else:
                 comp.synchronize()
                 eng.update_barrier(t)
@@ -495,14 +498,15 @@ def train_loop(lz, torch, eng, plan, built, payload, gbps, barrier):
         h3 = time.perf_counter()
         if ckpt:
             eng.wait_persisted(t)
-        return e0.elapsed_time(e1), (h1 - h0) * 1e3, (h2 - h1) * 1e3, (h3 - h0) * 1e3
+        fence_ms = f0.elapsed_time(f1) if ckpt and device_fence else 0.0
+        return e0.elapsed_time(e1), (h1 - h0) * 1e3, (h2 - h1) * 1e3, (h3 - h0) * 1e3, fence_ms
 
     barrier()
     for s in range(2):
         iteration(500 + s, False, True)
-    base = [iteration(510 + s, False, True)[3] for s in range(3)]
+    base = [iteration(510 + s, False, True)[3] for s in range(4)]
     iteration(520, True, True)
-    dev_fence = [iteration(530 + s, True, True) for s in range(3)]
+    dev_fence = [iteration(530 + s, True, True) for s in range(4)]
     iteration(540, True, False)
     host_fence = [iteration(550 + s, True, False) for s in range(2)]
     base_ms = statistics.mean(base)
@@ -511,6 +515,8 @@ def train_loop(lz, torch, eng, plan, built, payload, gbps, barrier):
     return {"t_fwd_bwd_ms": round(n_mm * per_mm, 2), "iter_no_ckpt_ms": round(base_ms, 2),
             "iter_ckpt_ms": round(it_ms, 2), "stall_ms": round(it_ms - base_ms, 2),
             "capture_host_ms": round(statistics.mean(x[1] for x in dev_fence), 3),
+            "fence_wait_ms": round(statistics.mean(x[4] for x in dev_fence), 3),
+            "stall_def_ms": round(statistics.mean(x[1] + x[4] for x in dev_fence), 3),
             "iter_overhead": round((it_ms - base_ms) / base_ms, 4),
             "host_fence": {"iter_ckpt_ms": round(it_host_ms, 2), "stall_ms": round(it_host_ms - base_ms, 2),
                            "iter_overhead": round((it_host_ms - base_ms) / base_ms, 4)},

@@ -16,7 +16,8 @@ from __future__ import annotations
 import dataclasses
 from typing import List, Tuple
 
-__all__ = ["Workload", "gpt2_small", "llama7b_shard", "llama_layer_sample", "sweep_class", "dense_model_shard"]
+__all__ = ["Workload", "gpt2_small", "llama7b_shard", "llama70b_shard", "llama_layer_sample", "sweep_class",
+           "dense_model_shard"]
 
 
 @dataclasses.dataclass
@@ -109,6 +110,32 @@ def llama7b_shard(seed: int = 7, layers: int = 32, vocab: int = 32000, dp: int =
         w.param_count *= dp
         w.topology = (dp, 1, 1, dp, 1)
         w.rank = (rank, 0, 0)
+    return w
+
+
+def _llama70b_tensors(layers=80, d=8192, kv=1024, ff=28672, vocab=32000):
+    out = [("embed_tokens", vocab * d)]
+    for l in range(layers):
+        p = f"layers.{l:02d}/"
+        out += [(p + "attn.q_proj", d * d), (p + "attn.k_proj", d * kv),
+                (p + "attn.v_proj", d * kv), (p + "attn.o_proj", d * d),
+                (p + "mlp.gate_proj", d * ff), (p + "mlp.up_proj", d * ff),
+                (p + "mlp.down_proj", ff * d),
+                (p + "input_norm", d), (p + "post_attn_norm", d)]
+    out += [("norm", d), ("lm_head", vocab * d)]
+    return out
+
+
+def llama70b_shard(seed: int = 70, layers: int = 10, dp: int = 8, rank: int = 0,
+                   name: str = "c4-llama70b") -> Workload:
+    """C4 (BASELINE.json configs[3]): one rank's ZeRO-style shard of a
+    LLaMA-2-70B-shaped model (d=8192, GQA k/v 8192x1024, ffn 28672, vocab
+    32000) over dp=8: 80/8 = 10 decoder layers plus embeddings, 4+12 B/param,
+    ~145 GB per GPU -- larger than any host pool it streams through."""
+    w = _model_state(name, _llama70b_tensors(layers=layers), 4, layers, "splitmix64", seed + rank)
+    w.param_count *= dp
+    w.topology = (dp, 1, 1, dp, 1)
+    w.rank = (rank, 0, 0)
     return w
 
 

@@ -55,3 +55,36 @@ def test_c2_fullsize_checksum_of_checksums(lz, oracle, tmp_path):
     print(f"C2 layers={layers}: {t.payload_bytes() / 1e9:.1f} GB, {nentries} entries equal to the oracle "
           f"(oracle {t_oracle:.1f} s, engine capture+hash {t_engine:.1f} s)")
     eng.close()
+
+
+def test_c4_streamed_70b_shard_checksum_of_checksums(lz, oracle, tmp_path):
+    """BASELINE.json configs[3]: one rank's ZeRO-style shard of a 70B model
+    over dp=8 (10 LLaMA-2-70B decoder layers + embeddings, 372 tensors,
+    145.3 GB) streamed through a 32 GiB pinned pool in 1 GiB segments with
+    backpressure (the shard and even its optimizer file are larger than the
+    pool). Every header entry must equal the oracle's."""
+    from paper_2406_10707_b200.workloads import llama70b_shard
+    assert lz.device_count() > 0
+    w = llama70b_shard()
+    pool = 32 << 30
+    if pool * 1.5 > _mem_available():
+        pytest.skip("host memory below 48 GiB")
+    thr = 1 << 20
+    expect = oracle.expected_headers(w, thr, threads=os.cpu_count() or 8)
+    built = lz.build_workload(w.write_spec(str(tmp_path / "c4.spec")), 0)
+    cfg = lz.EngineConfig(checkpoint_root=str(tmp_path / "ckpt"), host_buffer_bytes=pool, large_leaf_threshold=thr,
+                          fsync_on_finalize=False, flush_hash_only=True, stream_segment_bytes=1 << 30)
+    eng = lz.Engine(cfg, built.topo, built.rank)
+    t1 = time.time()
+    t = eng.capture(lz.plan_checkpoint(built.topo, built.model, built.step), built.tree, built.step)
+    eng.update_barrier(t)
+    eng.wait_persisted(t)
+    t_engine = time.time() - t1
+    got = {os.path.relpath(f, str(tmp_path / "ckpt")): [(e.key, e.offset, e.length, e.checksum) for e in h.entries]
+           for f, h in zip(t.shard_files(), eng.ticket_headers(t))}
+    assert got == expect
+    assert t.payload_bytes() > pool * 4
+    print(f"C4: {t.payload_bytes() / 1e9:.1f} GB through a {pool >> 30} GiB pool, "
+          f"{sum(len(v) for v in expect.values())} entries equal to the oracle ({t_engine:.1f} s)")
+    eng.close()
+    del built
