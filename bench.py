@@ -627,7 +627,20 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # NCCL prints its version line on fd 1 at the default WARN level,
+        # whatever NCCL_DEBUG_FILE says: keep fd 1 on stderr while the
+        # communicator is created eagerly (device_id), so stdout carries only
+        # the JSON line.
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            dist.barrier()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
     try:
         main_ours(args, rank, world, local_rank)
     finally:

@@ -26,7 +26,16 @@ if world > 1:
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(dev)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)  # NCCL's version line goes to fd 1 at the default WARN level
+    try:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        dist.barrier()
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
 
 
 def reduce(x, op):
