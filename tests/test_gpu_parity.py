@@ -624,3 +624,49 @@ def test_restores_files_written_by_the_reference_engine(gpu, oracle, cases, tmp_
         got = back.region_at(path).clone_bytes() if kind == "r" else back.blob_at(path)
         assert got == src[i].tobytes(), path
     eng.close()
+
+
+def test_restore_and_commit_entries_spanning_windows(gpu, oracle, tmp_path):
+    """Entries larger than the 512 MiB restore window (continued device
+    digests across windows, D2D scatter of window slices): a 1.2 GB and an
+    odd-sized ~700 MB region plus small ones, persisted, committed (GPU
+    validation), restored fresh and in place; restored bytes compared with
+    the sources by device FNV-1a (lz.device_fnv64, bit-exact vs the oracle in
+    test_gpu_fnv.py)."""
+    import ctypes as Cc
+    lz = gpu
+    sizes = {"big/w": (1200 << 20) + 3, "big/x": (700 << 20) - 13, "small/a": 4097, "small/b": 1 << 20}
+    tree = lz.StateTree()
+    regs = {}
+    s = Cc.c_void_p()
+    assert lz.dev.lzk_stream_create(0, 0, Cc.byref(s)) == 0
+    for i, (path, n) in enumerate(sizes.items()):
+        r = lz.DeviceRegion(n)
+        assert lz.dev.lzk_fill_splitmix(s, r.device_ptr, n, 77, i) == 0
+        regs[path] = r
+        tree.set_region(path, r)
+    assert lz.dev.lzk_stream_sync(s) == 0
+    lz.dev.lzk_stream_destroy(s)
+    want = dict(zip(sizes, lz.device_fnv64([(regs[p].device_ptr, n) for p, n in sizes.items()])))
+    total = sum(sizes.values())
+    topo = lz.ParallelTopology(1, 1, 1, 1, 1)
+    cfg = lz.EngineConfig(checkpoint_root=str(tmp_path), host_buffer_bytes=total + (256 << 20),
+                          large_leaf_threshold=1 << 20, fsync_on_finalize=False)
+    eng = lz.Engine(cfg, topo, lz.RankCoord())
+    t = eng.capture_file(str(tmp_path / "span.ckpt"), tree, 1)
+    eng.wait_persisted(t)
+    back = eng.restore_file(str(tmp_path / "span.ckpt"))
+    got = dict(zip(sizes, lz.device_fnv64([(back.region_at(p).device_ptr, n) for p, n in sizes.items()])))
+    assert got == want
+    del back
+    # in place: clobber the live regions, restore into them
+    for p, r in regs.items():
+        assert lz.dev.lzk_dev_memset(0, r.device_ptr, 0, sizes[p]) == 0
+    eng.restore_file(str(tmp_path / "span.ckpt"), into=tree)
+    got = dict(zip(sizes, lz.device_fnv64([(regs[p].device_ptr, n) for p, n in sizes.items()])))
+    assert got == want
+    # whole-file digest on the GPU (windows continued) == the oracle's fold
+    (rel, n, d), = lz.committed_record(t, str(tmp_path), digest=True)
+    assert n == os.path.getsize(tmp_path / "span.ckpt")
+    assert d == oracle.fnv64(np.fromfile(tmp_path / "span.ckpt", dtype=np.uint8))
+    eng.close()
