@@ -522,7 +522,11 @@ int launch_hash(cudaStream_t stream, int device, const lzk_hash_desc* d, uint32_
   if (any_long) {
     sc.S = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(dev) + table);
     sc.par = reinterpret_cast<uint8_t*>(sc.S + segs);
-    LZK_CK(cudaMemsetAsync(sc.par, 0, segs, stream));
+    const cudaError_t me = cudaMemsetAsync(sc.par, 0, segs, stream);
+    if (me != cudaSuccess) {
+      cudaFreeAsync(dev, stream);
+      return cuda_fail(me, "fnv: scratch memset");
+    }
   }
   const uint32_t grid = std::max(1u, std::min<uint32_t>((segs + kHashWarps - 1) / kHashWarps, ctas));
   if (any_long) {
@@ -543,9 +547,9 @@ int launch_hash(cudaStream_t stream, int device, const lzk_hash_desc* d, uint32_
     ++launches;
   }
   cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(dev, stream);  // stream-ordered: after the kernels above
   if (e != cudaSuccess) return cuda_fail(e, "lzk_fnv kernels launch");
   lzk_detail::launches.fetch_add(launches, std::memory_order_relaxed);
-  LZK_CK(cudaFreeAsync(dev, stream));
   return LZK_OK;
 }
 

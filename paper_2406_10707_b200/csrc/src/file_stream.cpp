@@ -139,6 +139,8 @@ void FileStreamer::ensure_states(size_t n) {
 void FileStreamer::stream(int fd, const std::filesystem::path& path, uint64_t end, const std::vector<Range>& ranges,
                           bool whole) {
   PhaseTrace tr("file_stream");
+  // a previous call that failed midway may have left DMAs in flight
+  ck(lzk_stream_sync(stream_), "file stream drain");
   const uint64_t wsize = std::min(kWindow, std::max<uint64_t>(end, 1));
   const size_t slots = size_t(std::min<uint64_t>(kWindows, (end + wsize - 1) / wsize));
   for (size_t k = 0; k < size_t(kWindows); ++k) {
@@ -176,6 +178,12 @@ void FileStreamer::stream(int fd, const std::filesystem::path& path, uint64_t en
   };
   std::thread reader;
   std::exception_ptr read_err;
+  struct JoinOnUnwind {  // an exception below must not destroy a joinable reader
+    std::thread& t;
+    ~JoinOnUnwind() {
+      if (t.joinable()) t.join();
+    }
+  } join_guard{reader};
   if (nwin) read_window(0);
   tr.mark("read0");
   for (size_t i = 0; i < nwin; ++i) {
