@@ -105,11 +105,19 @@ __device__ __forceinline__ uint4 ld_nc(const uint4* p) {
   return r;
 }
 
+// w >> (32 - k) as IMAD.HI on the FMA pipe (the kernel is bound by the ALU
+// pipe, where SHF would go).
+__device__ __forceinline__ uint32_t hi_shift(uint32_t w, uint32_t two_k) {
+  uint32_t r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(w), "r"(two_k));
+  return r;
+}
+
 __device__ __forceinline__ uint64_t fnv_word(uint64_t h, uint32_t w) {
   h = (h ^ (w & 0xffu)) * kPrime;
-  h = (h ^ ((w >> 8) & 0xffu)) * kPrime;
-  h = (h ^ ((w >> 16) & 0xffu)) * kPrime;
-  h = (h ^ (w >> 24)) * kPrime;
+  h = (h ^ (hi_shift(w, 1u << 24) & 0xffu)) * kPrime;
+  h = (h ^ (hi_shift(w, 1u << 16) & 0xffu)) * kPrime;
+  h = (h ^ hi_shift(w, 1u << 8)) * kPrime;
   return h;
 }
 
@@ -151,18 +159,21 @@ __device__ __forceinline__ void to_planes(const uint32_t* w, uint32_t* B) {
 }
 
 // Low bytes of one warp window: lane j holds bytes [32j, 32j + 32) in w.
-// Resolves planes 0..NP-1. `carry` (warp-uniform) holds the low byte at the
-// window start and is advanced past it (bits < NP). `valid` masks the lane's
-// positions that exist (partial last window). Outputs the low bytes at the
-// lane's offsets 0 and 16 (meaningful when NP == 8).
+// Resolves planes 0..NP-1. `carry[i]` (warp-uniform, 0 or 1) is bit i of the
+// low byte at the window start and is advanced past it. `valid` masks the
+// lane's positions that exist (partial last window). Outputs the low bytes
+// at the lane's offsets 0 and 16 (meaningful when NP == 8). The kernel is
+// bound by the ALU pipe, so bit bookkeeping uses multiplies (FMA pipe) and the
+// carries stay unpacked.
 template <int NP>
-__device__ __forceinline__ void scan_planes(const uint32_t* w, uint32_t& carry, uint32_t lt, uint32_t valid,
+__device__ __forceinline__ void scan_planes(const uint32_t* w, uint32_t* carry, uint32_t lt, uint32_t valid,
                                             uint32_t& l0, uint32_t& l16) {
   uint32_t B[8];
   to_planes(w, B);
-  uint32_t lstart = 0, lmid = 0;
+  uint32_t lstart = 0, q = 0;
   // plane i: l_i at each position = carry-in xor exclusive prefix-XOR of
-  // e_i; returns x_i = l_i ^ b_i.
+  // e_i; returns x_i = l_i ^ b_i. Bit 16 of l_i is bit 15 of the prefix
+  // xor the carry-in, so the offset-16 low byte is lstart ^ (q >> 15).
   auto plane = [&](int i, uint32_t e) -> uint32_t {
     uint32_t p = e & valid;
     p ^= p << 1;
@@ -171,12 +182,11 @@ __device__ __forceinline__ void scan_planes(const uint32_t* w, uint32_t& carry, 
     p ^= p << 8;
     p ^= p << 16;
     const uint32_t bal = __ballot_sync(0xffffffffu, p >> 31);
-    const uint32_t cin = (__popc(bal & lt) ^ (carry >> i)) & 1u;
-    carry ^= (__popc(bal) & 1u) << i;
-    const uint32_t l = (p << 1) ^ (0u - cin);
-    lstart |= cin << i;
-    lmid |= ((l >> 16) & 1u) << i;
-    return l ^ B[i];
+    const uint32_t cin = (__popc(bal & lt) ^ carry[i]) & 1u;
+    carry[i] ^= __popc(bal) & 1u;
+    lstart += cin * (1u << i);
+    q += (p & 0x8000u) * (1u << i);
+    return (p << 1) ^ (cin * 0xffffffffu) ^ B[i];
   };
   // column adder of y = 179 x (mod 256): column i sums x_i, x_{i-1},
   // x_{i-4}, x_{i-5}, x_{i-7} and the carries from column i-1.
@@ -211,7 +221,7 @@ __device__ __forceinline__ void scan_planes(const uint32_t* w, uint32_t& carry, 
     }
   }
   l0 = lstart;
-  l16 = lmid;
+  l16 = lstart ^ (q >> 15);
 }
 
 __device__ __forceinline__ uint64_t warp_sum(uint64_t v) {
@@ -239,7 +249,9 @@ __device__ uint64_t hash_range(const uint8_t* p, uint64_t n, uint64_t h, uint32_
   p += head;
   n -= head;
 
-  uint32_t carry = static_cast<uint32_t>(h) & 0xffu;
+  uint32_t carry[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) carry[i] = (static_cast<uint32_t>(h) >> i) & 1u;
   const uint64_t windows = n >> 10;
   if (windows) {
     const uint4* q = reinterpret_cast<const uint4*>(p) + 2 * lane;
@@ -359,7 +371,10 @@ __global__ void __launch_bounds__(kHashThreads) lzk_fnv_pass_kernel(const HashBa
     const uint8_t* src = reinterpret_cast<const uint8_t*>(it.d.src);
     const uint32_t head = head_len(it.d.src, it.d.len);
     const uint64_t hh = fold_bytes(it.d.seed, src, head);
-    uint32_t carry = (static_cast<uint32_t>(hh) ^ parity_prefix(sc.par, it.seg_begin, s, lane)) & ((1u << I) - 1u);
+    const uint32_t cin = (static_cast<uint32_t>(hh) ^ parity_prefix(sc.par, it.seg_begin, s, lane)) & ((1u << I) - 1u);
+    uint32_t carry[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) carry[i] = (cin >> i) & 1u;  // bit I starts at 0
     const uint4* q = reinterpret_cast<const uint4*>(src + head + uint64_t(s) * it.seglen) + 2 * lane;
     const uint64_t windows = it.seglen >> 10;
     uint4 a = ld_nc(q), b = ld_nc(q + 1);
@@ -373,13 +388,13 @@ __global__ void __launch_bounds__(kHashThreads) lzk_fnv_pass_kernel(const HashBa
       uint32_t l0, l16;
       scan_planes<I + 1>(w, carry, lt, 0xffffffffu, l0, l16);
     }
-    if (lane == 0) sc.par[t] |= static_cast<uint8_t>(carry & (1u << I));
+    if (lane == 0) sc.par[t] |= static_cast<uint8_t>(carry[I] << I);
   }
 }
 
 // Final pass: short ranges are hashed whole (result stored to out); every
 // segment of a long range is hashed from its incoming low byte.
-__global__ void __launch_bounds__(kHashThreads) lzk_fnv_kernel(const HashBatch batch, Scratch sc) {
+__global__ void __launch_bounds__(kHashThreads, 2) lzk_fnv_kernel(const HashBatch batch, Scratch sc) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt = (1u << lane) - 1u;
   const uint32_t nwarps = gridDim.x * kHashWarps;
