@@ -72,6 +72,8 @@ class FlushPipeline {
   // pool space): it ends Abandoned once the attached segments drain.
   void truncate_stream(uint64_t file_id);
   void enqueue_flush(uint64_t segment_id, uint64_t segment_offset, uint64_t length);
+  // B200 extension: several in-order chunks under one lock acquisition.
+  void enqueue_flush_spans(const std::vector<ChunkSpan>& spans);
   void abandon(uint64_t file_id);
   void inject_failure_after(uint64_t bytes);
   void drain();
@@ -140,6 +142,7 @@ class FlushPipeline {
   static constexpr uint64_t kRunBytes = 4ull << 20;
 
   void queue_writes(uint64_t id, FileRecord& f);
+  void enqueue_locked(std::unique_lock<std::mutex>& lk, uint64_t segment_id, uint64_t seg_offset, uint64_t length);
   void account(FileRecord& f, uint64_t from, uint64_t to);
   bool hashed_through(const FileRecord& f, uint64_t end) const;
   uint64_t register_common(std::filesystem::path path, CheckpointFileHeader header, FileDoneCallback on_done,

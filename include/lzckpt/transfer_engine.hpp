@@ -146,6 +146,13 @@ class TransferEngine {
   TransferEngine& operator=(const TransferEngine&) = delete;
 
   void set_chunk_callback(ChunkCallback cb) { chunk_cb_ = std::move(cb); }
+  // B200 extension: one call per completed device group, its chunks
+  // coalesced into contiguous spans (the engine feeds the flush this way;
+  // thousands of small tensors become a few notices). When set it replaces
+  // the per-chunk callback on the device path; the paced path and the
+  // reference's per-chunk contract are unchanged without it.
+  using SpanCallback = std::function<void(const std::vector<ChunkSpan>&)>;
+  void set_span_callback(SpanCallback cb) { span_cb_ = std::move(cb); }
   void set_torn_callback(TornCallback cb) { torn_cb_ = std::move(cb); }
 
   // Non-blocking: validates, enqueues the device work, returns.
@@ -228,6 +235,7 @@ class TransferEngine {
   int device_ = 0;
   lzk_stream* stream_ = nullptr;
   ChunkCallback chunk_cb_;
+  SpanCallback span_cb_;
   TornCallback torn_cb_;
 
   std::mutex opts_mu_;

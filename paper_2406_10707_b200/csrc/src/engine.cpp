@@ -45,7 +45,6 @@ struct ShardBuild {
   uint64_t shard_id = 0;
   std::filesystem::path path;
   CheckpointFileHeader header;
-  std::vector<LeafManifestEntry> manifest;
   std::shared_ptr<const std::vector<std::byte>> meta;
   struct Large {
     StateTree::RegionPtr region;
@@ -128,8 +127,9 @@ Engine::Engine(EngineConfig config, ParallelTopology topo, RankCoord rank)
   if (config_.large_leaf_threshold == 0) throw ConfigError("large-leaf threshold must be > 0");
   ck(lzk_stream_create(transfers_.device(), 0, &inline_stream_), "inline snapshot stream");
   transfers_.set_chunk_callback([this](uint64_t seg, uint64_t off, uint64_t len) {
-    flush_.enqueue_flush(seg, off, len);
+    flush_.enqueue_flush(seg, off, len);  // paced path
   });
+  transfers_.set_span_callback([this](const std::vector<ChunkSpan>& spans) { flush_.enqueue_flush_spans(spans); });
   transfers_.set_torn_callback([this](const CopyTask& t) { on_torn(t.ticket); });
   if (config_.stream_segment_bytes > 0) {
     if (config_.stream_segment_bytes > config_.host_buffer_bytes) {
@@ -161,6 +161,35 @@ Engine::~Engine() {
   }
   lzk_stream_destroy(inline_stream_);
   lzk_host_free(inline_buf_);
+}
+
+struct Engine::MetaPool {
+  std::mutex mu;
+  std::vector<std::unique_ptr<std::vector<std::byte>>> free;
+};
+
+StateTree::BlobPtr Engine::meta_buffer(uint64_t bytes, std::vector<std::byte>** writable) {
+  if (!meta_pool_) meta_pool_ = std::make_shared<MetaPool>();
+  std::unique_ptr<std::vector<std::byte>> v;
+  {
+    std::lock_guard lk(meta_pool_->mu);
+    if (!meta_pool_->free.empty()) {
+      v = std::move(meta_pool_->free.back());
+      meta_pool_->free.pop_back();
+    }
+  }
+  if (!v) v = std::make_unique<std::vector<std::byte>>();
+  v->resize(bytes);  // reused capacity: no allocation and no fill when the size repeats
+  *writable = v.get();
+  auto pool = meta_pool_;  // the blob may outlive the engine (tickets detach)
+  return StateTree::BlobPtr(v.release(), [pool](const std::vector<std::byte>* q) {
+    std::lock_guard lk(pool->mu);
+    if (pool->free.size() < 8) {
+      pool->free.emplace_back(const_cast<std::vector<std::byte>*>(q));
+    } else {
+      delete q;
+    }
+  });
 }
 
 // One gather launch for every small region leaf of the capture, then a sync:
@@ -262,30 +291,45 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
       b.shard_id = files[i].shard_id;
       b.path = files[i].path;
       const auto& leaves_i = files[i].leaves;
-      b.manifest.reserve(leaves_i.size());
-      for (auto& l : leaves_i) {
-        LeafManifestEntry e;
-        e.path = l.path;
-        e.is_region = l.region != nullptr;
-        e.size = l.size;
-        if (l.size < config_.large_leaf_threshold) {
-          e.inlined = true;
+      // __meta__ in one pass, serialize_leaf_manifest's layout
+      // (state_tree.cpp; reference state_tree.cpp:195-210): u32 n, then per
+      // leaf u32 len, path, u8 flags (1 region | 2 inlined), u64 size, and
+      // the inline bytes copied once from the pinned inline snapshot.
+      uint64_t total = 4, nlarge = 0;
+      for (const auto& l : leaves_i) {
+        const bool inl = l.size < config_.large_leaf_threshold;
+        total += 4 + l.path.size() + 1 + 8 + (inl ? l.size : 0);
+        nlarge += inl ? 0 : 1;
+      }
+      std::vector<std::byte>* mv = nullptr;
+      b.meta = meta_buffer(total, &mv);
+      std::byte* p = mv->data();
+      auto le = [&p](uint64_t v, int w) {
+        for (int k = 0; k < w; ++k) *p++ = std::byte(v >> (8 * k));
+      };
+      le(leaves_i.size(), 4);
+      b.header.entries.reserve(1 + nlarge);
+      b.header.entries.push_back({std::string(StateTree::kMetaKey), 0, total, 0});
+      b.larges.reserve(nlarge);
+      for (const auto& l : leaves_i) {
+        const bool inl = l.size < config_.large_leaf_threshold;
+        le(l.path.size(), 4);
+        std::memcpy(p, l.path.data(), l.path.size());
+        p += l.path.size();
+        *p++ = std::byte((l.region ? 1 : 0) | (inl ? 2 : 0));
+        le(l.size, 8);
+        if (inl) {
           if (l.region) {
             const uint64_t off = snap.regions[next_inline++].second;
-            e.inline_bytes.assign(inline_buf_ + off, inline_buf_ + off + l.size);
-          } else {
-            e.inline_bytes = *l.blob;
+            if (l.size) std::memcpy(p, inline_buf_ + off, l.size);
+          } else if (l.size) {
+            std::memcpy(p, l.blob->data(), l.size);
           }
+          p += l.size;
         } else {
           b.larges.push_back({l.region, l.blob, l.size});
+          b.header.entries.push_back({l.path, 0, l.size, 0});
         }
-        b.manifest.push_back(std::move(e));
-      }
-      b.meta = std::make_shared<const std::vector<std::byte>>(serialize_leaf_manifest(b.manifest));
-      b.manifest.clear();
-      b.header.entries.push_back({std::string(StateTree::kMetaKey), 0, b.meta->size(), 0});
-      for (const auto& l : leaves_i) {
-        if (l.size >= config_.large_leaf_threshold) b.header.entries.push_back({l.path, 0, l.size, 0});
       }
       uint64_t cursor = b.header.serialized_size();
       for (auto& e : b.header.entries) {

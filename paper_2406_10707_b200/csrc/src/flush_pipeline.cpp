@@ -206,57 +206,71 @@ void FlushPipeline::account(FileRecord& f, uint64_t from, uint64_t to) {
 void FlushPipeline::enqueue_flush(uint64_t segment_id, uint64_t seg_offset, uint64_t length) {
   {
     std::unique_lock lk(mu_);
-    if (!error_.empty()) return;
-    auto sit = seg_to_file_.find(segment_id);
-    if (sit == seg_to_file_.end()) {
-      fail_locked("chunk for unregistered segment " + std::to_string(segment_id));
-      return;
-    }
-    const uint64_t id = sit->second.first;
-    FileRecord& f = files_.at(id);
-    const SubSeg& sg = f.segs[sit->second.second];
-    const uint64_t offset = sg.off + seg_offset;
-    if (offset != f.enqueued || seg_offset + length > sg.len) {
-      fail_locked("out-of-order chunk for " + f.path.string());
-      return;
-    }
-    f.enqueued += length;
-    if (config_.discard) {
-      account(f, offset, offset + length);
-      if (f.enqueued == f.expected) maybe_finalize(lk, id);
-      release_in_order(lk);
-      return;
-    }
-
-    if (fail_after_ >= 0) {
-      const uint64_t writable = std::min<uint64_t>(length, uint64_t(fail_after_));
-      fail_after_ -= int64_t(writable);
-      if (writable < length) {
-        f.abandoned = true;
-        f.starve_from = std::min(f.starve_from, offset + writable);
-      }
-    }
-    queue_writes(id, f);
-    // Newly resident bytes feed the hash runs overlapping [offset, end).
-    const uint64_t end = offset + length;
-    size_t r = size_t(std::upper_bound(f.runs.begin(), f.runs.end(), offset,
-                                       [](uint64_t o, const HashRun& x) { return o < x.begin; }) -
-                      f.runs.begin());
-    if (r > 0) --r;
-    for (; r < f.runs.size() && f.runs[r].begin < end; ++r) {
-      HashRun& h = f.runs[r];
-      if (h.end <= offset) continue;
-      h.resident = std::max(h.resident, std::min(h.end, end));
-      if (!h.busy && h.resident > h.hashed) {
-        h.busy = true;
-        jobs_.push_back(Job{true, id, 0, 0, r});
-        ++f.jobs;
-      }
-    }
-    if (f.jobs == 0) maybe_finalize(lk, id);
-    release_in_order(lk);
+    enqueue_locked(lk, segment_id, seg_offset, length);
   }
   work_cv_.notify_all();
+}
+
+void FlushPipeline::enqueue_flush_spans(const std::vector<ChunkSpan>& spans) {
+  {
+    std::unique_lock lk(mu_);
+    for (const auto& c : spans) enqueue_locked(lk, c.segment_id, c.offset, c.length);
+  }
+  work_cv_.notify_all();
+}
+
+// One in-order chunk; under mu_ (maybe_finalize may drop and retake it).
+void FlushPipeline::enqueue_locked(std::unique_lock<std::mutex>& lk, uint64_t segment_id, uint64_t seg_offset,
+                                   uint64_t length) {
+  if (!error_.empty()) return;
+  auto sit = seg_to_file_.find(segment_id);
+  if (sit == seg_to_file_.end()) {
+    fail_locked("chunk for unregistered segment " + std::to_string(segment_id));
+    return;
+  }
+  const uint64_t id = sit->second.first;
+  FileRecord& f = files_.at(id);
+  const SubSeg& sg = f.segs[sit->second.second];
+  const uint64_t offset = sg.off + seg_offset;
+  if (offset != f.enqueued || seg_offset + length > sg.len) {
+    fail_locked("out-of-order chunk for " + f.path.string());
+    return;
+  }
+  f.enqueued += length;
+  if (config_.discard) {
+    account(f, offset, offset + length);
+    if (f.enqueued == f.expected) maybe_finalize(lk, id);
+    release_in_order(lk);
+    return;
+  }
+
+  if (fail_after_ >= 0) {
+    const uint64_t writable = std::min<uint64_t>(length, uint64_t(fail_after_));
+    fail_after_ -= int64_t(writable);
+    if (writable < length) {
+      f.abandoned = true;
+      f.starve_from = std::min(f.starve_from, offset + writable);
+    }
+  }
+  queue_writes(id, f);
+  // Newly resident bytes feed the hash runs overlapping [offset, end).
+  const uint64_t end = offset + length;
+  size_t r = size_t(std::upper_bound(f.runs.begin(), f.runs.end(), offset,
+                                     [](uint64_t o, const HashRun& x) { return o < x.begin; }) -
+                    f.runs.begin());
+  if (r > 0) --r;
+  for (; r < f.runs.size() && f.runs[r].begin < end; ++r) {
+    HashRun& h = f.runs[r];
+    if (h.end <= offset) continue;
+    h.resident = std::max(h.resident, std::min(h.end, end));
+    if (!h.busy && h.resident > h.hashed) {
+      h.busy = true;
+      jobs_.push_back(Job{true, id, 0, 0, r});
+      ++f.jobs;
+    }
+  }
+  if (f.jobs == 0) maybe_finalize(lk, id);
+  release_in_order(lk);
 }
 
 void FlushPipeline::abandon(uint64_t file_id) {

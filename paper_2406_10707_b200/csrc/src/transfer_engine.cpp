@@ -420,6 +420,8 @@ void TransferEngine::run_device_group(Group& g) {
       p.task->state.store(torn[i] ? CopyState::Torn : CopyState::Done);
     }
   }
+  std::vector<ChunkSpan> spans;
+  uint64_t delivered = 0;
   for (size_t i = 0; i < g.pieces.size(); ++i) {
     const Piece& p = g.pieces[i];
     CopyTask& t = *p.task;
@@ -427,8 +429,23 @@ void TransferEngine::run_device_group(Group& g) {
       if (torn[i] && torn_cb_) torn_cb_(t);
       if (t.final_for_segment) pool_.mark_filled(t.segment_id);
     }
+    if (span_cb_) {
+      const uint64_t off = t.dst_offset + p.offset;
+      if (!spans.empty() && spans.back().segment_id == t.segment_id &&
+          spans.back().offset + spans.back().length == off) {
+        spans.back().length += p.length;
+      } else {
+        spans.push_back(ChunkSpan{t.segment_id, off, p.length});
+      }
+      delivered += p.length;
+      continue;
+    }
     bytes_delivered_.fetch_add(p.length);
     if (chunk_cb_) chunk_cb_(t.segment_id, t.dst_offset + p.offset, p.length);
+  }
+  if (span_cb_) {
+    bytes_delivered_.fetch_add(delivered);
+    if (!spans.empty()) span_cb_(spans);
   }
 }
 
