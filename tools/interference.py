@@ -3,7 +3,9 @@ Times the bench's synthetic fwd/bwd (bf16 8192^3 GEMMs on a compute stream)
   A: alone,
   B: with a raw copy-engine D2H of the same bytes on a side stream (torch
      non_blocking copies into pinned memory; no engine, no host threads),
-  C: with an Engine capture of the C2 shard (the bench's configuration).
+  C: with an Engine capture of the C2 shard (the bench's configuration),
+  D: the same with every byte forced through lzk_gather_kernel (8 CTAs):
+     the SM time the kernel variant takes from the trainer.
 Prints one JSON line; B - A is hardware interference, C - B the engine's own.
     python tools/interference.py [layers]"""
 import json
@@ -64,7 +66,8 @@ def run(mode):
     torch.cuda.synchronize()
     h0 = time.perf_counter()
     t = None
-    if mode == "engine":
+    if mode in ("engine", "engine_kernel"):
+        eng.set_copy_variant(force_kernel=mode == "engine_kernel", force_copy_engine=False)
         t = eng.capture(plan, built.tree, int(time.time() * 1000) % 1000000 + 1)
     elif mode == "raw_dma":
         with torch.cuda.stream(side):
@@ -85,7 +88,7 @@ def run(mode):
 
 
 res = {}
-for mode in ("alone", "raw_dma", "engine", "alone", "raw_dma", "engine", "alone", "raw_dma", "engine"):
+for mode in ("alone", "raw_dma", "engine", "engine_kernel") * 3:
     g, wall = run(mode)
     res.setdefault(mode, []).append((g, wall))
 out = {"n_mm": n_mm, "per_mm_ms": round(per_mm, 4), "payload": payload}
@@ -94,5 +97,6 @@ for k, v in res.items():
               "wall_ms": round(statistics.median(x[1] for x in v), 2)}
 out["hw_interference_ms"] = round(out["raw_dma"]["gemm_ms"] - out["alone"]["gemm_ms"], 2)
 out["engine_extra_ms"] = round(out["engine"]["gemm_ms"] - out["raw_dma"]["gemm_ms"], 2)
+out["kernel_variant_extra_ms"] = round(out["engine_kernel"]["gemm_ms"] - out["alone"]["gemm_ms"], 2)
 print(json.dumps(out))
 eng.close()
