@@ -16,8 +16,8 @@ from __future__ import annotations
 import dataclasses
 from typing import List, Tuple
 
-__all__ = ["Workload", "gpt2_small", "llama7b_shard", "llama70b_shard", "llama_layer_sample", "sweep_class",
-           "dense_model_shard"]
+__all__ = ["Workload", "gpt2_small", "llama7b_shard", "llama13b_shard", "llama70b_shard", "llama_layer_sample",
+           "sweep_class", "dense_model_shard"]
 
 
 @dataclasses.dataclass
@@ -110,6 +110,18 @@ def llama7b_shard(seed: int = 7, layers: int = 32, vocab: int = 32000, dp: int =
         w.param_count *= dp
         w.topology = (dp, 1, 1, dp, 1)
         w.rank = (rank, 0, 0)
+    return w
+
+
+def llama13b_shard(seed: int = 13, layers: int = 5, dp: int = 8, rank: int = 0,
+                   name: str = "c3-llama13b") -> Workload:
+    """C3 (BASELINE.json configs[2]): one rank's shard of a LLaMA-13B-shaped
+    model (d=5120, ffn 13824, vocab 32000, 40 layers) over dp=8: 5 decoder
+    layers plus embeddings, 4+12 B/param, ~26 GB per GPU."""
+    w = _model_state(name, _llama7b_tensors(layers=layers, d=5120, ff=13824), 4, layers, "splitmix64", seed + rank)
+    w.param_count *= dp
+    w.topology = (dp, 1, 1, dp, 1)
+    w.rank = (rank, 0, 0)
     return w
 
 
