@@ -107,6 +107,14 @@ def all_cases():
         ("a", [("r", "emb", 3 * (1 << 20) + 7), ("r", "w", None)]),
         ("b", [("r", "m", 67 * (1 << 20) + 3), ("r", "v", 17 * (1 << 20) + 5), ("b", "s", 8), ("r", "rest", None)]),
     ], 1 << 20, seed=51))
+    # long, deep and non-ASCII paths: UTF-8 bytes order per component
+    # (std::string <), a 600-byte component, 24-level nesting
+    deep = "/".join(f"d{i:02d}" for i in range(24))
+    cases.append(_case("paths-utf8-deep", 60000, 2, [
+        ("a", [("r", "\u03bb/\u00e9t\u00e9", 5000), ("r", "\u03bb/e", 3000), ("r", "Z/\u4e2d\u6587", 4097),
+               ("r", "x" * 600, 8191), ("r", deep + "/leaf", 12000), ("b", "\u00ff", 7), ("r", "w", None)]),
+        ("b", [("r", "m\u00fcller/\U0001f600", 300000), ("r", "v", None)]),
+    ], 4096, seed=61))
     # mt19937_64 generator path (host fill) on a small model
     cases.append(_case("mt-small", 50000, 2, [
         ("a_params", [("r", "w", 60000), ("r", "b", None)]),
