@@ -193,7 +193,7 @@ class TransferEngine {
 
  private:
   struct Piece {
-    std::shared_ptr<CopyTask> task;
+    CopyTask* task = nullptr;  // owned by the ticket's task list until its last group is done
     uint64_t offset = 0;  // within the task
     uint64_t length = 0;
     bool last = false;

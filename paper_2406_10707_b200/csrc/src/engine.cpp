@@ -361,7 +361,7 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
     const uint64_t S = config_.stream_segment_bytes;
     std::vector<StreamJob> jobs;
     for (auto& b : builds) {
-      const uint64_t file_id = flush_.register_streamed_file(b.path, b.header,
+      const uint64_t file_id = flush_.register_streamed_file(b.path, std::move(b.header),
                                                              [this, weak](uint64_t, FlushFileState st) {
                                                                if (auto t = weak.lock()) on_file_done(t, st);
                                                              });
@@ -431,7 +431,7 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
   }
   for (auto& b : builds) {
     const Segment seg = pool_.reserve(b.payload, ticket->id_);  // backpressure blocks here
-    const uint64_t file_id = flush_.register_file(b.path, b.header, seg.id,
+    const uint64_t file_id = flush_.register_file(b.path, std::move(b.header), seg.id,
                                                   [this, weak](uint64_t, FlushFileState st) {
                                                     if (auto t = weak.lock()) on_file_done(t, st);
                                                   });
@@ -439,9 +439,11 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
       std::lock_guard tl(ticket->mu_);
       ticket->files_.push_back({b.path, file_id, seg.id});
     }
+    // one allocation for the file's tasks; each task shares the block
+    auto block = std::make_shared<std::vector<CopyTask>>(1 + b.larges.size());
     std::vector<std::shared_ptr<CopyTask>> tasks;
-    tasks.reserve(1 + b.larges.size());
-    auto meta = std::make_shared<CopyTask>();
+    tasks.reserve(block->size());
+    auto meta = std::shared_ptr<CopyTask>(block, block->data());
     meta->ticket = ticket->id_;
     meta->shard_id = b.shard_id;
     meta->source.host_blob = b.meta;
@@ -451,7 +453,7 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
     tasks.push_back(std::move(meta));
     uint64_t dst = b.meta->size();
     for (size_t k = 0; k < b.larges.size(); ++k) {
-      auto t = std::make_shared<CopyTask>();
+      auto t = std::shared_ptr<CopyTask>(block, block->data() + 1 + k);
       t->ticket = ticket->id_;
       t->shard_id = b.shard_id;
       t->source.region = b.larges[k].region;

@@ -206,13 +206,13 @@ void TransferEngine::submit_copies(uint64_t ticket, std::vector<std::shared_ptr<
     Group g;
     g.ticket = ticket;
     g.paced = true;
-    for (auto& t : tasks) g.pieces.push_back(Piece{t, 0, t->length, true});
+    for (auto& t : tasks) g.pieces.push_back(Piece{t.get(), 0, t->length, true});
     std::lock_guard lk(mu_);
     if (stopping_) throw Error("submit_copies: engine is shutting down");
     auto& tp = tickets_[ticket];
     tp.expected += tasks.size();
     tp.device_issued = false;
-    tp.tasks.insert(tp.tasks.end(), tasks.begin(), tasks.end());
+    tp.tasks.insert(tp.tasks.end(), std::make_move_iterator(tasks.begin()), std::make_move_iterator(tasks.end()));
     queue_.push_back(std::move(g));
     work_cv_.notify_one();
   } else {
@@ -223,7 +223,7 @@ void TransferEngine::submit_copies(uint64_t ticket, std::vector<std::shared_ptr<
     auto& tp = tickets_[ticket];
     tp.expected += tasks.size();
     tp.unissued += groups.size();
-    tp.tasks.insert(tp.tasks.end(), tasks.begin(), tasks.end());
+    tp.tasks.insert(tp.tasks.end(), std::make_move_iterator(tasks.begin()), std::make_move_iterator(tasks.end()));
     for (auto& g : groups) {
       g.ticket = ticket;
       issue_queue_.push_back(std::move(g));
@@ -256,8 +256,8 @@ void TransferEngine::build_groups(const std::vector<std::shared_ptr<CopyTask>>& 
     const bool use_ce = o.force_copy_engine || (!o.force_kernel && t->length >= o.ce_threshold);
     for (uint64_t off = 0; off < t->length; off += quantum) {
       const uint64_t n = std::min(quantum, t->length - off);
-      const bool extends = !cur.pieces.empty() && cur.pieces.back().task == t;
-      cur.pieces.push_back(Piece{t, off, n, off + n == t->length});
+      const bool extends = !cur.pieces.empty() && cur.pieces.back().task == t.get();
+      cur.pieces.push_back(Piece{t.get(), off, n, off + n == t->length});
       if (t->source.region) {
         auto& list = use_ce ? cur.dma : cur.kernel;
         if (extends && !list.empty()) {
@@ -362,13 +362,15 @@ void TransferEngine::worker_loop() {
     {
       std::lock_guard lk(mu_);
       --in_flight_;
+      bool all_done = false;
       for (const auto& p : g.pieces) {
         if (!p.last) continue;
         auto& tp = tickets_[p.task->ticket];
         ++tp.completed;
         if (p.task->state.load() == CopyState::Torn) tp.torn = true;
-        if (tp.completed == tp.expected) tp.tasks.clear();  // drop region references
+        all_done = tp.completed == tp.expected;
       }
+      if (all_done) tickets_[g.ticket].tasks.clear();  // drop region references (pieces point into them)
       if (g.done) {
         auto& tp = tickets_[g.ticket];
         if (tp.completed == tp.expected && tp.start_event && tp.unissued == 0) {
