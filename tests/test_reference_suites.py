@@ -38,3 +38,19 @@ def test_acceptance_criterion_1_consistency():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout + r.stderr[-2000:]
     assert "PASS" in r.stdout
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_program_all_criteria(tmp_path):
+    """The reference's whole acceptance program (tests/acceptance_main.cpp,
+    compiled in place by tests/reftests/Makefile): criteria 1-4 (consistency
+    round trips and tears, buffer pool, file format, commit safety) run on the
+    B200 engine; criteria 5-10 run the reference's discrete-event simulator
+    (out of scope here, compiled from the reference tree as it is)."""
+    exe = os.path.join(ROOT, "tests", "reftests", "bin", "acceptance_full")
+    assert os.path.exists(exe), f"{exe} missing: build with `make -C tests/reftests` where /root/reference exists"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=1500, cwd=str(tmp_path))
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("criterion")]
+    assert len(lines) == 10 and all(": PASS" in l for l in lines), "\n".join(lines)
+    assert "acceptance: all criteria PASS" in r.stdout
