@@ -261,10 +261,13 @@ def main_ours(args, rank, world, local_rank):
                 ms.append(max(dms, hms))
             variants[name] = round(payload / (statistics.mean(ms) * 1e-3) / 1e9, 3)
             log(f"[bench] rank {rank}: variant {name}: {variants[name]} GB/s")
-        best = max(("gather_kernel", "copy_engine", "hybrid"), key=lambda k: variants[k])
-        eng.set_copy_variant(**{"gather_kernel": dict(force_kernel=True),
-                                "copy_engine": dict(force_copy_engine=True),
-                                "hybrid": dict(ce_threshold=2 << 20)}[best])
+        # The headline times the product default (hybrid: kernel below 2 MiB,
+        # copy engines above), the configuration a trainer runs: forcing every
+        # byte through the kernel takes ~7 % of the trainer's GEMM throughput
+        # (tools/interference.py) even on boxes where it edges out the DMA
+        # engines. All three variants are reported in variants_gbps.
+        best = "hybrid"
+        eng.set_copy_variant(ce_threshold=2 << 20)
 
         # ---- timed region ----
         for s in range(args.warmup):
@@ -520,7 +523,8 @@ def train_loop(lz, torch, eng, plan, built, payload, gbps, barrier):
             "iter_overhead": round((it_ms - base_ms) / base_ms, 4),
             "host_fence": {"iter_ckpt_ms": round(it_host_ms, 2), "stall_ms": round(it_host_ms - base_ms, 2),
                            "iter_overhead": round((it_host_ms - base_ms) / base_ms, 4)},
-            "fence": "update_barrier_on_stream (device-side)", "gemm": "bf16 8192^3 torch.matmul x%d" % n_mm}
+            "fence": "update_barrier_on_stream (device-side)", "variant": "hybrid (engine default)",
+            "gemm": "bf16 8192^3 torch.matmul x%d" % n_mm}
 
 
 def e2e_persisted(lz, torch, dev, tmp, args, world=1, rank=0):

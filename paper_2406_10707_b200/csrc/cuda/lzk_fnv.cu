@@ -424,22 +424,38 @@ __global__ void __launch_bounds__(kHashThreads, 2) lzk_fnv_kernel(const HashBatc
   }
 }
 
-// h = S_0, then h = P^len_s * h + S_s over the remaining segments.
+// h = S_0, then h = P^len_s * h + S_s over the remaining segments. Every
+// segment is an affine map h -> M h + A (segment 0: M = 0, A = S_0); a lane
+// composes a contiguous block of segments, then a shuffle-down tree composes
+// the 32 block maps in order (the composition is associative, not
+// commutative). One warp per long range.
 __global__ void lzk_fnv_combine_kernel(const HashBatch batch, Scratch sc) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
   for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < batch.n; i += nwarps) {
     const HashItem it = batch.it[i];
-    if (it.nseg == 1 || lane != 0) continue;
+    if (it.nseg == 1) continue;
     const uint64_t head = head_len(it.d.src, it.d.len);
-    const uint64_t pseg = pow64(kPrime, it.seglen);
-    uint64_t h = sc.S[it.seg_begin];
-    for (uint32_t s = 1; s < it.nseg; ++s) {
-      const uint64_t off = head + uint64_t(s) * it.seglen;
-      const uint64_t n = min(it.seglen, it.d.len - off);
-      h = (n == it.seglen ? pseg : pow64(kPrime, n)) * h + sc.S[it.seg_begin + s];
+    const uint64_t last = it.d.len - head - uint64_t(it.nseg - 1) * it.seglen;
+    const uint64_t pseg = pow64(kPrime, it.seglen), plast = pow64(kPrime, last);
+    const uint32_t per = (it.nseg + 31u) / 32u;
+    const uint32_t b0 = min(it.nseg, lane * per), b1 = min(it.nseg, b0 + per);
+    uint64_t M = 1, A = 0;  // identity
+    for (uint32_t s = b0; s < b1; ++s) {
+      const uint64_t m = s == 0 ? 0 : (s + 1 == it.nseg ? plast : pseg);
+      M = m * M;
+      A = m * A + sc.S[it.seg_begin + s];
     }
-    *reinterpret_cast<uint64_t*>(it.d.out) = h;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {  // lane L holds blocks [L, L + 2*off) after this step
+      const uint64_t Mr = __shfl_down_sync(0xffffffffu, M, off);
+      const uint64_t Ar = __shfl_down_sync(0xffffffffu, A, off);
+      if (lane + off < 32) {
+        A = Mr * A + Ar;  // right o left
+        M = Mr * M;
+      }
+    }
+    if (lane == 0) *reinterpret_cast<uint64_t*>(it.d.out) = A;
   }
 }
 
