@@ -610,7 +610,8 @@ int lzckpt_engine_prepare(lzckpt_engine* e, const lzckpt_model_spec* model, lzck
     if (rep) {
       for (const auto& f : rep->files) j["files"].push_back({f.relative_path, f.length, f.digest});
     }
-    const std::string out = j.dump();
+    // leaf keys in `detail` are user strings: never throw on invalid UTF-8
+    const std::string out = j.dump(-1, ' ', false, nlohmann::json::error_handler_t::replace);
     *needed = out.size() + 1;
     if (json && cap >= out.size() + 1) std::memcpy(json, out.c_str(), out.size() + 1);
   });
