@@ -115,6 +115,16 @@ enum class CopyState { Queued, Copying, Done, Torn };
 struct CopySource {
   std::shared_ptr<DeviceRegion> region;
   std::shared_ptr<const std::vector<std::byte>> host_blob;
+  // B200 extension: host bytes in pinned memory kept alive by `host_keep`
+  // (the engine's __meta__, whose inline leaves the gather kernel writes in
+  // place). A task has exactly one of region / host_blob / host_ptr.
+  const std::byte* host_ptr = nullptr;
+  uint64_t host_size = 0;
+  std::shared_ptr<const void> host_keep;
+
+  bool is_host() const { return host_blob != nullptr || host_ptr != nullptr; }
+  const std::byte* host_data() const { return host_blob ? host_blob->data() : host_ptr; }
+  uint64_t host_bytes() const { return host_blob ? host_blob->size() : host_size; }
 };
 
 struct CopyTask {

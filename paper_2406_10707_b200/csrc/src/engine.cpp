@@ -45,7 +45,8 @@ struct ShardBuild {
   uint64_t shard_id = 0;
   std::filesystem::path path;
   CheckpointFileHeader header;
-  std::shared_ptr<const std::vector<std::byte>> meta;
+  std::shared_ptr<const std::byte> meta;  // pinned, mapped (MetaPool)
+  uint64_t meta_size = 0;
   struct Large {
     StateTree::RegionPtr region;
     StateTree::BlobPtr blob;
@@ -74,11 +75,6 @@ struct Pinned {
 
 }  // namespace
 
-struct Engine::InlineSnapshot {
-  std::vector<std::pair<DeviceRegion*, uint64_t>> regions;  // (region, staging offset)
-  uint64_t bytes = 0;
-  Pinned staging;
-};
 
 const char* to_string(TicketStatus s) {
   switch (s) {
@@ -160,58 +156,52 @@ Engine::~Engine() {
     }
   }
   lzk_stream_destroy(inline_stream_);
-  lzk_host_free(inline_buf_);
 }
 
 struct Engine::MetaPool {
   std::mutex mu;
-  std::vector<std::unique_ptr<std::vector<std::byte>>> free;
+  std::vector<std::pair<std::byte*, uint64_t>> free;  // pinned blocks, capacity
+  ~MetaPool() {
+    for (auto& [p, n] : free) lzk_host_free(p);
+  }
 };
 
-StateTree::BlobPtr Engine::meta_buffer(uint64_t bytes, std::vector<std::byte>** writable) {
+std::shared_ptr<const std::byte> Engine::meta_buffer(uint64_t bytes) {
   if (!meta_pool_) meta_pool_ = std::make_shared<MetaPool>();
-  std::unique_ptr<std::vector<std::byte>> v;
+  std::byte* p = nullptr;
+  uint64_t cap = 0;
   {
     std::lock_guard lk(meta_pool_->mu);
-    if (!meta_pool_->free.empty()) {
-      v = std::move(meta_pool_->free.back());
-      meta_pool_->free.pop_back();
+    auto& fl = meta_pool_->free;
+    for (size_t i = 0; i < fl.size(); ++i) {
+      if (fl[i].second >= bytes) {
+        std::tie(p, cap) = fl[i];
+        fl.erase(fl.begin() + long(i));
+        break;
+      }
     }
   }
-  if (!v) v = std::make_unique<std::vector<std::byte>>();
-  v->resize(bytes);  // reused capacity: no allocation and no fill when the size repeats
-  *writable = v.get();
-  auto pool = meta_pool_;  // the blob may outlive the engine (tickets detach)
-  return StateTree::BlobPtr(v.release(), [pool](const std::vector<std::byte>* q) {
+  if (!p) {
+    cap = std::max<uint64_t>(bytes, 1);
+    void* q = nullptr;
+    ck(lzk_host_alloc(cap, LZK_HOST_MAPPED, &q), "meta buffer");
+    p = static_cast<std::byte*>(q);
+  }
+  auto pool = meta_pool_;  // the buffer may outlive the engine (tickets detach)
+  return std::shared_ptr<const std::byte>(p, [pool, cap](const std::byte* q) {
     std::lock_guard lk(pool->mu);
     if (pool->free.size() < 8) {
-      pool->free.emplace_back(const_cast<std::vector<std::byte>*>(q));
+      pool->free.emplace_back(const_cast<std::byte*>(q), cap);
     } else {
-      delete q;
+      lzk_host_free(const_cast<std::byte*>(q));
     }
   });
-}
-
-// One gather launch for every small region leaf of the capture, then a sync:
-// the bytes are captured before capture() returns, as the reference's
-// synchronous clone (engine.cpp:138-143) guarantees.
-void Engine::snapshot_inline_leaves(InlineSnapshot& snap) const {
-  if (snap.regions.empty()) return;
-  std::vector<lzk_copy_desc> d;
-  d.reserve(snap.regions.size());
-  for (auto& [r, off] : snap.regions) {
-    if (r->size() == 0) continue;
-    d.push_back(lzk_copy_desc{reinterpret_cast<uint64_t>(r->device_ptr()),
-                              reinterpret_cast<uint64_t>(inline_buf_ + off), r->size()});
-  }
-  ck(lzk_gather_d2h(inline_stream_, d.data(), uint32_t(d.size()), config_.snapshot.kernel_ctas),
-     "inline leaf gather");
-  ck(lzk_stream_sync(inline_stream_), "inline leaf gather sync");
 }
 
 std::shared_ptr<CaptureTicket> Engine::capture(const CheckpointPlan& plan, const StateTree& state,
                                                uint64_t step) {
   const auto t0 = std::chrono::steady_clock::now();
+  PhaseTrace ftr("capture-flatten");
   const auto& shards = plan.shards(flat_rank(topo_, rank_));
   const auto names = state.top_level_names();
   if (names.size() != shards.size()) {
@@ -225,14 +215,15 @@ std::shared_ptr<CaptureTicket> Engine::capture(const CheckpointPlan& plan, const
   for (size_t i = 0; i < shards.size(); ++i) {
     files[i].path = shard_path(config_.checkpoint_root, step, shards[i]);
     files[i].shard_id = shards[i].shard_id;
-    files[i].leaves = state.flatten_child(names[i]);
+    files[i].leaves = state.flatten_child_shared(names[i]);
     uint64_t sum = 0;
-    for (const auto& l : files[i].leaves) sum += l.size;
+    for (const auto& l : *files[i].leaves) sum += l.size;
     if (sum != shards[i].size_bytes) {
       throw ConfigError("subtree '" + names[i] + "' holds " + std::to_string(sum) + " bytes but shard " +
                         shards[i].filename() + " expects " + std::to_string(shards[i].size_bytes));
     }
   }
+  ftr.mark("flatten");
   return capture_impl(files, step, t0);
 }
 
@@ -241,10 +232,10 @@ std::shared_ptr<CaptureTicket> Engine::capture_file(const std::filesystem::path&
   const auto t0 = std::chrono::steady_clock::now();
   std::vector<FileSpec> files(1);
   files[0].path = path;
-  files[0].leaves = state.flatten();
+  files[0].leaves = std::make_shared<const std::vector<StateTree::FlatLeaf>>(state.flatten());
   uint64_t sum = 0;
-  for (const auto& l : files[0].leaves) sum += l.size;
-  if (files[0].leaves.empty()) throw ConfigError("capture_file: empty state tree");
+  for (const auto& l : *files[0].leaves) sum += l.size;
+  if (files[0].leaves->empty()) throw ConfigError("capture_file: empty state tree");
   (void)sum;
   return capture_impl(files, step, t0);
 }
@@ -253,9 +244,8 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
                                                     std::chrono::steady_clock::time_point t0) {
   PhaseTrace tr;
   std::vector<ShardBuild> builds(files.size());
-  InlineSnapshot snap;
   for (auto& f : files) {
-    for (const auto& l : f.leaves) {
+    for (const auto& l : *f.leaves) {
       if (l.path == StateTree::kMetaKey) {
         throw DuplicatePath("top-level leaf name '" + l.path + "' is reserved");
       }
@@ -263,47 +253,34 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
         throw ConfigError("leaf '" + l.path + "' lives on device " + std::to_string(l.region->device()) +
                           ", engine on " + std::to_string(transfers_.device()));
       }
-      if (l.region && l.size < config_.large_leaf_threshold) {
-        snap.regions.emplace_back(l.region.get(), snap.bytes);
-        snap.bytes += l.size;
-      }
     }
   }
+  tr.mark("flatten+validate");
 
   {
-    std::lock_guard il(inline_mu_);
-    if (snap.bytes > inline_cap_) {
-      lzk_host_free(inline_buf_);
-      inline_buf_ = nullptr;
-      inline_cap_ = 0;
-      void* p = nullptr;
-      ck(lzk_host_alloc(snap.bytes, LZK_HOST_MAPPED, &p), "inline staging");
-      inline_buf_ = static_cast<std::byte*>(p);
-      inline_cap_ = snap.bytes;
-    }
-    tr.mark("flatten+validate");
-    snapshot_inline_leaves(snap);
-    tr.mark("inline_gather");
-
-    size_t next_inline = 0;
+    std::lock_guard il(inline_mu_);  // one inline gather at a time (inline_stream_)
+    // Small region leaves go straight from HBM into their slots of __meta__
+    // (pinned, mapped), by ONE gather launch for the whole capture; the
+    // reference clones each under a lock (engine.cpp:138-143).
+    std::vector<lzk_copy_desc> inl;
     for (size_t i = 0; i < files.size(); ++i) {
       ShardBuild& b = builds[i];
       b.shard_id = files[i].shard_id;
       b.path = files[i].path;
-      const auto& leaves_i = files[i].leaves;
+      const auto& leaves_i = *files[i].leaves;
       // __meta__ in one pass, serialize_leaf_manifest's layout
       // (state_tree.cpp; reference state_tree.cpp:195-210): u32 n, then per
       // leaf u32 len, path, u8 flags (1 region | 2 inlined), u64 size, and
-      // the inline bytes copied once from the pinned inline snapshot.
+      // the inline bytes (host blobs copied here, regions by the kernel).
       uint64_t total = 4, nlarge = 0;
       for (const auto& l : leaves_i) {
-        const bool inl = l.size < config_.large_leaf_threshold;
-        total += 4 + l.path.size() + 1 + 8 + (inl ? l.size : 0);
-        nlarge += inl ? 0 : 1;
+        const bool inl_leaf = l.size < config_.large_leaf_threshold;
+        total += 4 + l.path.size() + 1 + 8 + (inl_leaf ? l.size : 0);
+        nlarge += inl_leaf ? 0 : 1;
       }
-      std::vector<std::byte>* mv = nullptr;
-      b.meta = meta_buffer(total, &mv);
-      std::byte* p = mv->data();
+      b.meta = meta_buffer(total);
+      b.meta_size = total;
+      std::byte* p = const_cast<std::byte*>(b.meta.get());
       auto le = [&p](uint64_t v, int w) {
         for (int k = 0; k < w; ++k) *p++ = std::byte(v >> (8 * k));
       };
@@ -312,16 +289,17 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
       b.header.entries.push_back({std::string(StateTree::kMetaKey), 0, total, 0});
       b.larges.reserve(nlarge);
       for (const auto& l : leaves_i) {
-        const bool inl = l.size < config_.large_leaf_threshold;
+        const bool inl_leaf = l.size < config_.large_leaf_threshold;
         le(l.path.size(), 4);
         std::memcpy(p, l.path.data(), l.path.size());
         p += l.path.size();
-        *p++ = std::byte((l.region ? 1 : 0) | (inl ? 2 : 0));
+        *p++ = std::byte((l.region ? 1 : 0) | (inl_leaf ? 2 : 0));
         le(l.size, 8);
-        if (inl) {
+        if (inl_leaf) {
           if (l.region) {
-            const uint64_t off = snap.regions[next_inline++].second;
-            if (l.size) std::memcpy(p, inline_buf_ + off, l.size);
+            if (l.size) {
+              inl.push_back({reinterpret_cast<uint64_t>(l.region->device_ptr()), reinterpret_cast<uint64_t>(p), l.size});
+            }
           } else if (l.size) {
             std::memcpy(p, l.blob->data(), l.size);
           }
@@ -338,9 +316,16 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
       }
       b.payload = cursor - b.header.serialized_size();
     }
+    tr.mark("meta+header");
+    if (!inl.empty()) {
+      // synchronous: the bytes are captured before capture() returns
+      ck(lzk_gather_d2h(inline_stream_, inl.data(), uint32_t(inl.size()), config_.snapshot.kernel_ctas),
+         "inline leaf gather");
+      ck(lzk_stream_sync(inline_stream_), "inline leaf gather sync");
+    }
+    tr.mark("inline_gather");
   }
 
-  tr.mark("meta+header");
   auto ticket = std::shared_ptr<CaptureTicket>(new CaptureTicket());
   {
     std::lock_guard lk(mu_);
@@ -375,7 +360,7 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
         StateTree::BlobPtr blob;
         uint64_t size;
       };
-      std::vector<Src> srcs{{nullptr, b.meta, b.meta->size()}};
+      std::vector<Src> srcs{{nullptr, nullptr, b.meta_size}};  // [0] = __meta__ (pinned)
       for (const auto& l : b.larges) srcs.push_back({l.region, l.blob, l.size});
       size_t si = 0;
       uint64_t soff = 0;
@@ -393,7 +378,13 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
             t->ticket = ticket->id_;
             t->shard_id = b.shard_id;
             t->source.region = src.region;
-            t->source.host_blob = src.region ? nullptr : src.blob;
+            if (si == 0) {
+              t->source.host_ptr = b.meta.get();
+              t->source.host_size = b.meta_size;
+              t->source.host_keep = b.meta;
+            } else if (!src.region) {
+              t->source.host_blob = src.blob;
+            }
             t->src_offset = soff;
             t->length = n;
             t->dst_offset = filled;
@@ -446,12 +437,14 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
     auto meta = std::shared_ptr<CopyTask>(block, block->data());
     meta->ticket = ticket->id_;
     meta->shard_id = b.shard_id;
-    meta->source.host_blob = b.meta;
-    meta->length = b.meta->size();
+    meta->source.host_ptr = b.meta.get();
+    meta->source.host_size = b.meta_size;
+    meta->source.host_keep = b.meta;
+    meta->length = b.meta_size;
     meta->segment_id = seg.id;
     meta->final_for_segment = b.larges.empty();
     tasks.push_back(std::move(meta));
-    uint64_t dst = b.meta->size();
+    uint64_t dst = b.meta_size;
     for (size_t k = 0; k < b.larges.size(); ++k) {
       auto t = std::shared_ptr<CopyTask>(block, block->data() + 1 + k);
       t->ticket = ticket->id_;

@@ -182,8 +182,11 @@ void TransferEngine::submit_copies(uint64_t ticket, std::vector<std::shared_ptr<
     if (t->length == 0) throw Error("submit_copies: zero-length copy");
     const bool has_region = static_cast<bool>(t->source.region);
     const bool has_blob = static_cast<bool>(t->source.host_blob);
-    if (has_region == has_blob) throw Error("submit_copies: task needs exactly one source");
-    const uint64_t src_size = has_region ? t->source.region->size() : t->source.host_blob->size();
+    const bool has_ptr = t->source.host_ptr != nullptr;
+    if (int(has_region) + int(has_blob) + int(has_ptr) != 1) {
+      throw Error("submit_copies: task needs exactly one source");
+    }
+    const uint64_t src_size = has_region ? t->source.region->size() : t->source.host_bytes();
     if (t->src_offset + t->length > src_size) throw Error("submit_copies: source range out of bounds");
     if (has_region && t->source.region->device() != device_) {
       throw ConfigError("submit_copies: region lives on device " +
@@ -402,10 +405,10 @@ void TransferEngine::run_device_group(Group& g) {
   uint64_t blob = 0;
   for (const auto& p : g.pieces) {
     const CopyTask& t = *p.task;
-    if (!t.source.host_blob) continue;
+    if (!t.source.is_host()) continue;
     const Segment seg = pool_.segment_info(t.segment_id);
     std::memcpy(pool_.segment_data(seg) + t.dst_offset + p.offset,
-                t.source.host_blob->data() + t.src_offset + p.offset, p.length);
+                t.source.host_data() + t.src_offset + p.offset, p.length);
     blob += p.length;
   }
   const bool device_ok = !g.issue_failed && lzk_event_sync(g.done) == LZK_OK;
@@ -472,7 +475,7 @@ void TransferEngine::run_paced_group(Group& g) {
         ok = lzk_memcpy_d2h(r.device(), dst + done,
                             static_cast<const std::byte*>(r.device_ptr()) + t.src_offset + done, n) == LZK_OK;
       } else {
-        std::memcpy(dst + done, t.source.host_blob->data() + t.src_offset + done, n);
+        std::memcpy(dst + done, t.source.host_data() + t.src_offset + done, n);
       }
       pace_point_ += std::chrono::nanoseconds(int64_t(double(n) / channel_.bandwidth_Bps * 1e9));
       std::this_thread::sleep_until(pace_point_);
