@@ -365,15 +365,14 @@ void TransferEngine::worker_loop() {
     {
       std::lock_guard lk(mu_);
       --in_flight_;
-      bool all_done = false;
+      // a group holds pieces of one ticket only
+      auto& tg = tickets_[g.ticket];
       for (const auto& p : g.pieces) {
         if (!p.last) continue;
-        auto& tp = tickets_[p.task->ticket];
-        ++tp.completed;
-        if (p.task->state.load() == CopyState::Torn) tp.torn = true;
-        all_done = tp.completed == tp.expected;
+        ++tg.completed;
+        if (p.task->state.load(std::memory_order_relaxed) == CopyState::Torn) tg.torn = true;
       }
-      if (all_done) tickets_[g.ticket].tasks.clear();  // drop region references (pieces point into them)
+      if (tg.completed == tg.expected) tg.tasks.clear();  // drop region references (pieces point into them)
       if (g.done) {
         auto& tp = tickets_[g.ticket];
         if (tp.completed == tp.expected && tp.start_event && tp.unissued == 0) {
