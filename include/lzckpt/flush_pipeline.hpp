@@ -59,15 +59,20 @@ class FlushPipeline {
   FlushPipeline(const FlushPipeline&) = delete;
   FlushPipeline& operator=(const FlushPipeline&) = delete;
 
+  // B200 extension `payload_pad`: the payload starts `payload_pad` bytes
+  // into the segment (the engine places large leaves 4 KiB-aligned in host
+  // memory; the copy engines of some hosts lose ~8 % on misaligned
+  // destinations). Chunk offsets stay relative to the segment start.
   uint64_t register_file(std::filesystem::path path, CheckpointFileHeader header,
-                         uint64_t segment_id, FileDoneCallback on_done = {});
+                         uint64_t segment_id, FileDoneCallback on_done = {}, uint64_t payload_pad = 0);
   // B200 extension — streaming through a pool smaller than the file: the
   // payload arrives in consecutive segments attached as they are reserved;
   // every segment but the last is released as soon as its bytes are written
   // and hashed, the last one after the header (file bytes are unchanged).
   uint64_t register_streamed_file(std::filesystem::path path, CheckpointFileHeader header,
                                   FileDoneCallback on_done = {});
-  void attach_segment(uint64_t file_id, uint64_t segment_id, uint64_t payload_offset);
+  void attach_segment(uint64_t file_id, uint64_t segment_id, uint64_t payload_offset, uint64_t payload_pad = 0,
+                      uint64_t payload_len = 0);  // 0: the whole segment
   // Gives up on the rest of a streamed file (a capture that could not get
   // pool space): it ends Abandoned once the attached segments drain.
   void truncate_stream(uint64_t file_id);
@@ -103,7 +108,8 @@ class FlushPipeline {
     uint64_t id = 0;
     uint64_t off = 0;
     uint64_t len = 0;
-    std::byte* base = nullptr;
+    std::byte* base = nullptr;  // payload byte `off` (segment start + pad)
+    uint64_t pad = 0;           // payload offset within the segment
     uint64_t accounted = 0;  // written + starved bytes inside this segment
     bool released = false;
   };

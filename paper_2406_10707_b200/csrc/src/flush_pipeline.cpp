@@ -125,15 +125,15 @@ uint64_t FlushPipeline::register_common(std::filesystem::path path, CheckpointFi
 }
 
 uint64_t FlushPipeline::register_file(std::filesystem::path path, CheckpointFileHeader header,
-                                      uint64_t segment_id, FileDoneCallback on_done) {
+                                      uint64_t segment_id, FileDoneCallback on_done, uint64_t payload_pad) {
   const uint64_t expected = header.payload_end() - header.serialized_size();
   if (expected == 0) throw Error("flush file with empty payload: " + path.string());
   const Segment seg = pool_.segment_info(segment_id);
-  if (seg.length != expected) {
+  if (payload_pad == 0 ? seg.length != expected : seg.length < payload_pad + expected) {
     throw Error("segment length does not match file payload for " + path.string());
   }
   FileRecord f;
-  f.segs.push_back(SubSeg{segment_id, 0, expected, pool_.segment_data(seg), 0, false});
+  f.segs.push_back(SubSeg{segment_id, 0, expected, pool_.segment_data(seg) + payload_pad, payload_pad, 0, false});
   f.attached = expected;
   return register_common(std::move(path), std::move(header), std::move(on_done), f);
 }
@@ -144,17 +144,20 @@ uint64_t FlushPipeline::register_streamed_file(std::filesystem::path path, Check
   return register_common(std::move(path), std::move(header), std::move(on_done), f);
 }
 
-void FlushPipeline::attach_segment(uint64_t file_id, uint64_t segment_id, uint64_t payload_offset) {
+void FlushPipeline::attach_segment(uint64_t file_id, uint64_t segment_id, uint64_t payload_offset,
+                                   uint64_t payload_pad, uint64_t payload_len) {
   const Segment seg = pool_.segment_info(segment_id);
+  const uint64_t len = payload_len ? payload_len : seg.length - payload_pad;
+  if (payload_pad + len > seg.length) throw Error("attach_segment: payload exceeds the segment");
   std::lock_guard lk(mu_);
   auto it = files_.find(file_id);
   if (it == files_.end()) throw Error("attach_segment: unknown flush file");
   FileRecord& f = it->second;
-  if (payload_offset != f.attached || payload_offset + seg.length > f.expected) {
+  if (payload_offset != f.attached || payload_offset + len > f.expected) {
     throw Error("attach_segment: segments must tile the payload in order for " + f.path.string());
   }
-  f.segs.push_back(SubSeg{segment_id, payload_offset, seg.length, pool_.segment_data(seg), 0, false});
-  f.attached += seg.length;
+  f.segs.push_back(SubSeg{segment_id, payload_offset, len, pool_.segment_data(seg) + payload_pad, payload_pad, 0, false});
+  f.attached += len;
   seg_to_file_.emplace(segment_id, std::make_pair(file_id, f.segs.size() - 1));
   release_order_.emplace_back(file_id, f.segs.size() - 1);
 }
@@ -231,8 +234,12 @@ void FlushPipeline::enqueue_locked(std::unique_lock<std::mutex>& lk, uint64_t se
   const uint64_t id = sit->second.first;
   FileRecord& f = files_.at(id);
   const SubSeg& sg = f.segs[sit->second.second];
-  const uint64_t offset = sg.off + seg_offset;
-  if (offset != f.enqueued || seg_offset + length > sg.len) {
+  if (seg_offset < sg.pad) {
+    fail_locked("chunk before the payload of " + f.path.string());
+    return;
+  }
+  const uint64_t offset = sg.off + (seg_offset - sg.pad);
+  if (offset != f.enqueued || seg_offset - sg.pad + length > sg.len) {
     fail_locked("out-of-order chunk for " + f.path.string());
     return;
   }
