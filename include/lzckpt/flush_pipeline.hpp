@@ -37,7 +37,7 @@ struct FlushConfig {
   bool fsync_on_finalize = true;
   // B200-host extensions
   unsigned threads = 0;              // worker pool size; 0 = auto (<= 8)
-  uint64_t write_piece = 8ull << 20; // max bytes per pwrite job
+  uint64_t write_piece = 32ull << 20; // max bytes per pwrite job
   // Host-memory tier only: no file is created, nothing is hashed or written;
   // a segment is released as soon as all of its bytes are resident. For
   // measuring the D2H snapshot stage on shards larger than local storage.
@@ -46,6 +46,13 @@ struct FlushConfig {
   // header is built, but nothing is written (full-size parity checks on
   // shards larger than local storage).
   bool hash_only = false;
+  // Durable files: the block-aligned interior of every write piece goes to
+  // the device with O_DIRECT (through an aligned per-thread bounce buffer;
+  // ring addresses are laid out for DMA alignment, not file alignment), the
+  // partial edge blocks and the header stay buffered. Falls back to buffered
+  // writes where O_DIRECT is unavailable. (B200 hosts' local disk: 4.1-4.3
+  // GB/s O_DIRECT vs 2.2 buffered.)
+  bool direct_io = true;
 };
 
 enum class FlushFileState { Pending, Persisted, Abandoned, Discarded };
@@ -130,6 +137,7 @@ class FlushPipeline {
     std::vector<HashRun> runs;
     size_t entries_done = 0;
     int fd = -1;
+    int dfd = -1;  // O_DIRECT descriptor of the same file (-1: buffered only)
     bool abandoned = false;
     bool finalizing = false;
     bool finalized = false;

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cerrno>
+#include <cstdlib>
 #include <cstring>
 #include <utility>
 
@@ -40,6 +41,47 @@ void pwrite_all(int fd, const std::byte* p, uint64_t n, uint64_t off, const std:
     off += uint64_t(w);
     n -= uint64_t(w);
   }
+}
+
+constexpr uint64_t kBlock = 4096;  // O_DIRECT alignment (offset, length, buffer)
+
+// Writes [off, off + n) with O_DIRECT from an aligned per-thread bounce
+// buffer; off and n are block multiples. Returns false when the file system
+// refuses O_DIRECT for this write (the caller falls back to buffered).
+bool pwrite_direct(int dfd, const std::byte* p, uint64_t n, uint64_t off, uint64_t piece,
+                   const std::filesystem::path& path) {
+  struct Bounce {
+    void* p = nullptr;
+    uint64_t cap = 0;
+    ~Bounce() { std::free(p); }
+  };
+  thread_local Bounce b;
+  const uint64_t want = std::max<uint64_t>(kBlock, (std::min(piece, n) + kBlock - 1) & ~(kBlock - 1));
+  if (b.cap < want) {
+    std::free(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+    if (posix_memalign(&b.p, kBlock, want) != 0) return false;
+    b.cap = want;
+  }
+  while (n) {
+    const uint64_t k = std::min(n, b.cap);
+    std::memcpy(b.p, p, k);
+    uint64_t done = 0;
+    while (done < k) {
+      const ssize_t w = ::pwrite(dfd, static_cast<std::byte*>(b.p) + done, k - done, off_t(off + done));
+      if (w < 0) {
+        if (errno == EINTR) continue;
+        if (errno == EINVAL && done == 0) return false;  // not supported here
+        throw IoError("write failed for " + path.string() + ": " + std::strerror(errno));
+      }
+      done += uint64_t(w);
+    }
+    p += k;
+    off += k;
+    n -= k;
+  }
+  return true;
 }
 
 }  // namespace
@@ -66,6 +108,7 @@ FlushPipeline::~FlushPipeline() {
   for (auto& t : workers_) t.join();
   for (auto& [id, f] : files_) {
     if (f.fd >= 0) ::close(f.fd);
+    if (f.dfd >= 0) ::close(f.dfd);
   }
 }
 
@@ -82,6 +125,9 @@ uint64_t FlushPipeline::register_common(std::filesystem::path path, CheckpointFi
     std::filesystem::create_directories(path.parent_path(), ec);
     f.fd = ::open(path.c_str(), O_CREAT | O_WRONLY | O_TRUNC | O_CLOEXEC, 0644);
     if (f.fd < 0) throw IoError("cannot create " + path.string() + ": " + std::strerror(errno));
+    if (config_.direct_io && config_.fsync_on_finalize && config_.storage_bandwidth_Bps <= 0) {
+      f.dfd = ::open(path.c_str(), O_WRONLY | O_DIRECT | O_CLOEXEC);  // -1: buffered only
+    }
   }
   f.path = std::move(path);
   f.on_done = std::move(on_done);
@@ -171,7 +217,8 @@ void FlushPipeline::truncate_stream(uint64_t file_id) {
   f.expected = f.attached;
   if (f.segs.empty()) {  // nothing ever attached: done right away
     if (f.fd >= 0) ::close(f.fd);
-    f.fd = -1;
+    if (f.dfd >= 0) ::close(f.dfd);
+    f.fd = f.dfd = -1;
     f.finalizing = f.finalized = true;
     f.state = FlushFileState::Abandoned;
     --pending_files_;
@@ -383,7 +430,17 @@ void FlushPipeline::run_write(FileRecord& f, const Job& j, const std::byte* src)
     }
     std::this_thread::sleep_until(until);
   }
-  pwrite_all(f.fd, src, j.length, f.header_size + j.offset, f.path);
+  const uint64_t off = f.header_size + j.offset, end = off + j.length;
+  if (f.dfd >= 0) {
+    // block-aligned interior through O_DIRECT, partial edge blocks buffered
+    const uint64_t a = (off + kBlock - 1) & ~(kBlock - 1), b = end & ~(kBlock - 1);
+    if (b > a && pwrite_direct(f.dfd, src + (a - off), b - a, a, config_.write_piece, f.path)) {
+      if (a > off) pwrite_all(f.fd, src, a - off, off, f.path);
+      if (end > b) pwrite_all(f.fd, src + (b - off), end - b, b, f.path);
+      return;
+    }
+  }
+  pwrite_all(f.fd, src, j.length, off, f.path);
   // Durable files: start writeback of this piece now. The kernel's own
   // background writeback only begins past dirty_background_ratio (~19 GB on
   // the B200 hosts), so without this a whole checkpoint is written back
@@ -515,8 +572,9 @@ void FlushPipeline::maybe_finalize(std::unique_lock<std::mutex>& lk, uint64_t id
     }
   }
   if (f.fd >= 0) ::close(f.fd);
+  if (f.dfd >= 0) ::close(f.dfd);
   lk.lock();
-  f.fd = -1;
+  f.fd = f.dfd = -1;
   if (!err.empty()) {
     fail_locked(err);
     return;
