@@ -600,10 +600,10 @@ def e2e_persisted(lz, torch, dev, tmp, args, world=1, rank=0):
             "path": "capture -> update_barrier -> wait_persisted, fsync, local disk", "steps": len(times),
             "commit_gbps": round(payload / commit_s / 1e9, 3),
             "commit_seconds": round(commit_s, 3),
-            "commit_reads": "from the disk: durable writes use O_DIRECT, so the files are not in the page cache",
+            "commit_reads": "from the disk with O_DIRECT (durable writes bypass the page cache, so fresh files are cold)",
             "commit_path": "2PC (N>1: votes over torch.distributed): each file read once, entry checksums + whole-file digest on the GPU",
             "restore_gbps": round(payload / restore_s / 1e9, 3), "restore_spot_check": ok,
-            "restore_reads": "page cache (warmed by the commit's reads)",
+            "restore_reads": "per 512 MiB window: the page cache when mincore shows it resident, else O_DIRECT",
             "restore_path": "parallel pread into pinned windows -> one DMA per window -> device FNV check -> D2D to regions"}
 
 

@@ -2,6 +2,7 @@
 #include "file_stream.hpp"
 
 #include <fcntl.h>
+#include <sys/mman.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -62,6 +63,29 @@ void pread_all(int fd, void* dst, uint64_t n, uint64_t off, const std::filesyste
     off += uint64_t(r);
     n -= uint64_t(r);
   }
+}
+
+// O_DIRECT read of [off, off + n) into an aligned buffer (off aligned to
+// 4 KiB; n rounded up to a block, a short read at EOF is fine). Returns
+// false when the file system refuses O_DIRECT (caller reads buffered).
+bool pread_direct(int dfd, void* dst, uint64_t n, uint64_t off, uint64_t file_end) {
+  constexpr uint64_t kBlock = 4096;
+  if (dfd < 0 || off % kBlock || reinterpret_cast<uintptr_t>(dst) % kBlock) return false;
+  const uint64_t want = (n + kBlock - 1) & ~(kBlock - 1);
+  auto* d = static_cast<char*>(dst);
+  uint64_t done = 0;
+  while (done < n) {
+    const ssize_t r = ::pread(dfd, d + done, want - done, off_t(off + done));
+    if (r < 0) {
+      if (errno == EINTR) continue;
+      if (errno == EINVAL && done == 0) return false;
+      throw IoError("read failed: " + std::string(std::strerror(errno)));
+    }
+    if (r == 0) break;
+    done += uint64_t(r);
+  }
+  if (done < n && off + done < file_end) throw IoError("short O_DIRECT read");
+  return true;
 }
 
 struct Fd {
@@ -138,6 +162,28 @@ void FileStreamer::ensure_states(size_t n) {
 
 void FileStreamer::stream(int fd, const std::filesystem::path& path, uint64_t end, const std::vector<Range>& ranges,
                           bool whole) {
+  Fd direct{::open(path.c_str(), O_RDONLY | O_DIRECT | O_CLOEXEC)};  // -1: buffered reads only
+  const int dfd = direct.fd;
+  // Page-cache residency per window (mincore on a read-only mapping): a
+  // window mostly in the cache is read through it, anything else with
+  // O_DIRECT (durable writes bypass the cache, so fresh checkpoints are cold).
+  void* map = end ? ::mmap(nullptr, end, PROT_READ, MAP_SHARED, fd, 0) : MAP_FAILED;
+  struct Unmap {
+    void* p;
+    uint64_t n;
+    ~Unmap() {
+      if (p != MAP_FAILED) ::munmap(p, n);
+    }
+  } unmap{map, end};
+  auto mostly_cached = [&](uint64_t off, uint64_t len) {
+    if (map == MAP_FAILED || len == 0) return true;
+    const uint64_t pg = 4096, npg = (len + pg - 1) / pg;
+    std::vector<unsigned char> v(npg);
+    if (::mincore(static_cast<char*>(map) + off, len, v.data()) != 0) return true;
+    uint64_t res = 0;
+    for (unsigned char c : v) res += c & 1;
+    return res * 2 >= npg;
+  };
   PhaseTrace tr("file_stream");
   // a previous call that failed midway may have left DMAs in flight
   ck(lzk_stream_sync(stream_), "file stream drain");
@@ -171,9 +217,15 @@ void FileStreamer::stream(int fd, const std::filesystem::path& path, uint64_t en
     if (w.used) ck(lzk_event_sync(w.done), "file stream window reuse");
     const uint64_t off = uint64_t(i) * wsize, len = std::min(wsize, end - off);
     const uint64_t piece = 64ull << 20;
+    const bool use_direct = dfd >= 0 && !mostly_cached(off, len);
     parallel_for(size_t((len + piece - 1) / piece), 8, [&](size_t k) {
-      const uint64_t o = uint64_t(k) * piece;
-      pread_all(fd, w.buf + o, std::min(piece, len - o), off + o, path);
+      const uint64_t o = uint64_t(k) * piece, n = std::min(piece, len - o);
+      // O_DIRECT first (files written by the flush are usually not in the
+      // page cache); windows are page-aligned and piece offsets 64 MiB
+      // multiples. The round-up of the last piece stays inside the window.
+      if (!(use_direct && o + ((n + 4095) & ~uint64_t(4095)) <= w.cap && pread_direct(dfd, w.buf + o, n, off + o, end))) {
+        pread_all(fd, w.buf + o, n, off + o, path);
+      }
     });
   };
   std::thread reader;
