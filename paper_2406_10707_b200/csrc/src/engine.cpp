@@ -186,13 +186,14 @@ std::shared_ptr<const std::byte> Engine::meta_buffer(uint64_t bytes) {
   uint64_t cap = 0;
   {
     std::lock_guard lk(meta_pool_->mu);
-    auto& fl = meta_pool_->free;
+    auto& fl = meta_pool_->free;  // best fit
+    size_t best = fl.size();
     for (size_t i = 0; i < fl.size(); ++i) {
-      if (fl[i].second >= bytes) {
-        std::tie(p, cap) = fl[i];
-        fl.erase(fl.begin() + long(i));
-        break;
-      }
+      if (fl[i].second >= bytes && (best == fl.size() || fl[i].second < fl[best].second)) best = i;
+    }
+    if (best < fl.size()) {
+      std::tie(p, cap) = fl[best];
+      fl.erase(fl.begin() + long(best));
     }
   }
   if (!p) {
