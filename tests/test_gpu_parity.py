@@ -29,6 +29,11 @@ VARIANTS = {
     # pool far smaller than the files: every file streams through odd-sized
     # segments with backpressure (C4 mode), bytes must not change
     "streaming": {"stream_segment_bytes": 1_000_003, "host_buffer_bytes": 3_000_009, "chunk_quantum": 262_147},
+    # durable files: O_DIRECT interior + buffered edge blocks + header last +
+    # fsync (FlushConfig::direct_io)
+    "durable": {"fsync_on_finalize": True},
+    "durable-streaming": {"fsync_on_finalize": True, "stream_segment_bytes": 1_000_003,
+                          "host_buffer_bytes": 3_000_009, "chunk_quantum": 262_147},
 }
 
 
@@ -43,8 +48,9 @@ def run_capture(lz, w, thr, root, spec_dir, **knobs):
     built = lz.build_workload(spec, 0)
     knobs = dict(knobs)
     pool = knobs.pop("host_buffer_bytes", max(2 * built.bytes, 1 << 20) + (8 << 20))
+    knobs.setdefault("fsync_on_finalize", False)
     cfg = lz.EngineConfig(checkpoint_root=str(root), host_buffer_bytes=pool,
-                          large_leaf_threshold=thr, fsync_on_finalize=False, **knobs)
+                          large_leaf_threshold=thr, **knobs)
     eng = lz.Engine(cfg, built.topo, built.rank)
     t = eng.capture(lz.plan_checkpoint(built.topo, built.model, built.step), built.tree, built.step)
     eng.update_barrier(t)
