@@ -348,13 +348,19 @@ def main_ours(args, rank, world, local_rank):
                 "capture_host_ms": round(statistics.mean(cap_ms), 3),
                 "variants_gbps": variants,
                 "roofline": {"bound": "pcie-host-link", "achieved": round(per_gpu, 3), "peak": PCIE_GEN5_X16_GBPS,
-                             "unit": "GB/s", "frac": round(per_gpu / PCIE_GEN5_X16_GBPS, 4), "traffic": None,
+                             "unit": "GB/s", "frac": round(per_gpu / PCIE_GEN5_X16_GBPS, 4),
+                             "traffic": None,  # copy-engine DMAs: not visible to ncu kernel metrics
                              "peak_measured_dma": link["dma_gbps"],
                              "frac_of_measured_dma": round(per_gpu / link["dma_gbps"], 4),
                              "kernel": {"name": "lzk_gather_kernel", "achieved": kernel_gbps,
                                         "frac": round(kernel_gbps / PCIE_GEN5_X16_GBPS, 4),
                                         "peak_measured_sm_store": link["sm_store_gbps"],
-                                        "frac_of_measured_sm_store": round(kernel_gbps / link["sm_store_gbps"], 4)},
+                                        "frac_of_measured_sm_store": round(kernel_gbps / link["sm_store_gbps"], 4),
+                                        # one `ncu --set full` capture of a 62.92 MB launch
+                                        # (profiles/r01_gather_kernel_ncu.md, v3): DRAM read +
+                                        # write per launch vs the algorithmic bytes
+                                        "traffic": 62.92e6 + 0.43e6, "algorithmic_bytes_per_launch": 62.92e6,
+                                        "ncu_profile": "profiles/r01_gather_kernel_ncu.md"},
                              "link_probe": link["how"],
                              "algorithmic_bytes_per_step": payload},
                 "stall": stall,
