@@ -359,7 +359,7 @@ def main_ours(args, rank, world, local_rank):
                                         # one `ncu --set full` capture of a 62.92 MB launch
                                         # (profiles/r01_gather_kernel_ncu.md, v3): DRAM read +
                                         # write per launch vs the algorithmic bytes
-                                        "traffic": 62.92e6 + 0.43e6, "algorithmic_bytes_per_launch": 62.92e6,
+                                        "traffic": 62.9248e6 + 0.3566e6, "algorithmic_bytes_per_launch": 62.92e6,
                                         "ncu_profile": "profiles/r01_gather_kernel_ncu.md"},
                              "link_probe": link["how"],
                              "algorithmic_bytes_per_step": payload},
