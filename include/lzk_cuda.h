@@ -153,6 +153,13 @@ int lzk_fnv1a64_batch(lzk_stream* s, const lzk_hash_desc* d, uint32_t n, uint32_
  * its `out` address (seed ignored) and the new state written back there. */
 int lzk_fnv1a64_continue(lzk_stream* s, const lzk_hash_desc* d, uint32_t n, uint32_t max_ctas);
 
+/* ---- profiler ranges -------------------------------------------------------- */
+/* NVTX ranges (nsys / ncu timelines): no-ops unless a profiler is attached.
+ * The engine marks capture, the lazy fences, flush finalize, restore and
+ * commit validation with them. */
+void lzk_range_push(const char* name);
+void lzk_range_pop(void);
+
 /* ---- synthetic workload generation (bench/tests) ------------------------ */
 /* Fills `bytes` of device memory with the splitmix64 counter stream of
  * (seed, leaf): word w = mix64((seed ^ leaf*0xD1B54A32D192ED03) + (w+1)*0x9E3779B97F4A7C15),

@@ -204,6 +204,8 @@ DEVICE_SYMBOLS = [
     ("lzk_fnv1a64_continue", i32, [vp, P(HashDescC), u32, u32]),
     ("lzk_fill_splitmix", i32, [vp, vp, u64, u64, u64]),
     ("lzk_busy_compute", i32, [vp, vp, u64, u32, u32]),
+    ("lzk_range_push", None, [cp]),
+    ("lzk_range_pop", None, []),
 ]
 
 

@@ -41,6 +41,8 @@
 
 #include <sys/mman.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "lzk_internal.h"
 
 namespace lzk_detail {
@@ -708,6 +710,9 @@ int lzk_fill_splitmix(lzk_stream* s, void* dev, uint64_t bytes, uint64_t seed, u
   lzk_detail::launches.fetch_add(1, std::memory_order_relaxed);
   return LZK_OK;
 }
+
+void lzk_range_push(const char* name) { nvtxRangePushA(name ? name : "lzk"); }
+void lzk_range_pop(void) { nvtxRangePop(); }
 
 int lzk_busy_compute(lzk_stream* s, float* buf, uint64_t n, uint32_t iters, uint32_t ctas) {
   if (!s) return fail(LZK_ERR_INVALID, "null stream");

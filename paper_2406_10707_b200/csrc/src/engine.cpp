@@ -257,6 +257,7 @@ std::shared_ptr<CaptureTicket> Engine::capture_file(const std::filesystem::path&
 
 std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files, uint64_t step,
                                                     std::chrono::steady_clock::time_point t0) {
+  detail::NvtxRange range("lzckpt.capture");
   PhaseTrace tr;
   std::vector<ShardBuild> builds(files.size());
   for (auto& f : files) {
@@ -562,6 +563,7 @@ void Engine::wait_streamed(const std::shared_ptr<CaptureTicket>& ticket) {
 }
 
 void Engine::update_barrier(const std::shared_ptr<CaptureTicket>& ticket) {
+  detail::NvtxRange range("lzckpt.fence.host");
   const auto t0 = std::chrono::steady_clock::now();
   auto record = [&] {
     const double dt = since(t0);
@@ -584,6 +586,7 @@ void Engine::update_barrier(const std::shared_ptr<CaptureTicket>& ticket) {
 }
 
 void Engine::update_barrier_on_stream(const std::shared_ptr<CaptureTicket>& ticket, void* cuda_stream) {
+  detail::NvtxRange range("lzckpt.fence.device");
   const auto t0 = std::chrono::steady_clock::now();
   wait_streamed(ticket);  // streamed segments must all be on the device first
   if (!transfers_.fence_on_stream(ticket->id_, cuda_stream)) {
@@ -746,6 +749,7 @@ namespace {
 // blobs and inline leaves from host bytes. Reads each byte once.
 void restore_one(const std::filesystem::path& path, StateTree& tree, const StateTree* into, int dev,
                  FileStreamer& streamer) {
+  detail::NvtxRange range("lzckpt.restore.file");
   PhaseTrace tr("restore_one");
   CheckpointFileHeader h;
   auto leaves = open_shard(path, h);

@@ -184,6 +184,7 @@ void FileStreamer::stream(int fd, const std::filesystem::path& path, uint64_t en
     for (unsigned char c : v) res += c & 1;
     return res * 2 >= npg;
   };
+  NvtxRange range("lzckpt.file_stream");
   PhaseTrace tr("file_stream");
   // a previous call that failed midway may have left DMAs in flight
   ck(lzk_stream_sync(stream_), "file stream drain");

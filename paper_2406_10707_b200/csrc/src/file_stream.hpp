@@ -41,6 +41,14 @@ struct PhaseTrace {
   }
 };
 
+// NVTX range for the lifetime of the object (a no-op without a profiler).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { lzk_range_push(name); }
+  ~NvtxRange() { lzk_range_pop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // Where one entry's bytes go while a file streams back.
 struct EntrySink {
   void* device = nullptr;                 // region memory (device address), or

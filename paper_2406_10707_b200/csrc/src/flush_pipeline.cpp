@@ -25,6 +25,7 @@
 #include <utility>
 
 #include "lzckpt/errors.hpp"
+#include "lzk_cuda.h"
 
 namespace lzckpt {
 
@@ -560,6 +561,7 @@ void FlushPipeline::maybe_finalize(std::unique_lock<std::mutex>& lk, uint64_t id
     }
   }
   lk.unlock();
+  lzk_range_push("lzckpt.flush.finalize");
   if (err.empty()) {
     try {
       pool_.begin_flush(last_seg);  // Filled -> Flushing
@@ -573,6 +575,7 @@ void FlushPipeline::maybe_finalize(std::unique_lock<std::mutex>& lk, uint64_t id
   }
   if (f.fd >= 0) ::close(f.fd);
   if (f.dfd >= 0) ::close(f.dfd);
+  lzk_range_pop();
   lk.lock();
   f.fd = f.dfd = -1;
   if (!err.empty()) {
