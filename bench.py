@@ -255,7 +255,7 @@ def main_ours(args, rank, world, local_rank):
             barrier()
             one_step(1)
             ms = []
-            for s in range(2):
+            for s in range(3):
                 barrier()
                 dms, hms, payload, _ = one_step(2 + s)
                 ms.append(max(dms, hms))
