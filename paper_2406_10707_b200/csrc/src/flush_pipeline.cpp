@@ -126,7 +126,10 @@ uint64_t FlushPipeline::register_common(std::filesystem::path path, CheckpointFi
     std::filesystem::create_directories(path.parent_path(), ec);
     f.fd = ::open(path.c_str(), O_CREAT | O_WRONLY | O_TRUNC | O_CLOEXEC, 0644);
     if (f.fd < 0) throw IoError("cannot create " + path.string() + ": " + std::strerror(errno));
-    if (config_.direct_io && config_.fsync_on_finalize && config_.storage_bandwidth_Bps <= 0) {
+    // O_DIRECT pays off for bulk payloads; small files (the reference's
+    // verify trials write thousands) stay on the plain buffered path
+    if (config_.direct_io && config_.fsync_on_finalize && config_.storage_bandwidth_Bps <= 0 &&
+        f.expected >= (4ull << 20)) {
       f.dfd = ::open(path.c_str(), O_WRONLY | O_DIRECT | O_CLOEXEC);  // -1: buffered only
     }
   }
