@@ -8,7 +8,7 @@
 // Underneath it is B200-native:
 //  * DeviceRegion owns (or wraps) real HBM;
 //  * unpaced submissions are cut into groups on the caller (host metadata
-//    only) and issued by a per-engine issuer thread onto a low-priority
+//    only) and issued by a per-engine issuer thread onto a dedicated
 //    snapshot stream: tensors below SnapshotOptions::ce_threshold go through
 //    ONE multi-tensor gather kernel launch per group (lzk_gather_d2h), larger
 //    ones through the copy engines (lzk_ce_copy_d2h); a CUDA event closes
@@ -105,7 +105,11 @@ struct SnapshotOptions {
   uint64_t ce_threshold = 2ull << 20; // tasks >= this go to the copy engines
   uint32_t kernel_ctas = 8;           // gather kernel grid: 4 saturate PCIe for every size class
   uint64_t group_bytes = 256ull << 20; // bytes per completion event (and max DMA size)
-  int stream_priority = 1;            // > 0: below default (compute) priority
+  // > 0: the least priority, < 0: the greatest. CUDA's least priority IS the
+  // default (0), so the snapshot stream never ranks below an ordinary compute
+  // stream; a trainer that wants its kernels scheduled ahead of the gather
+  // kernel creates its own stream at a greater (negative) priority.
+  int stream_priority = 1;
   bool force_kernel = false;          // every region chunk through the gather kernel
   bool force_copy_engine = false;     // every region chunk through the copy engines
 };

@@ -546,6 +546,8 @@ int lzk_stream_create(int device, int priority, lzk_stream** out) {
   if (int rc = use_device(device)) return rc;
   int least = 0, greatest = 0;
   LZK_CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  // least == 0 == the default priority on current GPUs: there is nothing below
+  // an ordinary stream, so priority > 0 means "no boost", not "demoted".
   int p = priority > 0 ? least : (priority < 0 ? greatest : 0);
   auto* s = new (std::nothrow) lzk_stream();
   if (!s) return fail(LZK_ERR_NOMEM, "stream");
