@@ -184,6 +184,17 @@ class TransferEngine {
   // after every copy of `ticket`. Returns false when the ticket's copies are
   // not device-issued (paced channel); the caller then waits on the host.
   bool fence_on_stream(uint64_t ticket, void* cuda_stream);
+  // Producer ordering (capture on a trainer stream). Records an event on
+  // `producer_stream` now (NULL = the legacy default stream); the ticket's
+  // device work waits for it, so the snapshot reads what the trainer queued
+  // before capture() and never a half-written tensor. `inline_descs` (small
+  // leaves gathered straight into their __meta__ slots) then run first on the
+  // snapshot stream, and `inline_regions` get the same torn verdict as large
+  // leaves (the reference clones them at capture, engine.cpp:138-143; here
+  // that read is deferred behind the producer instead of blocking the
+  // trainer). Call before the ticket's first submit_copies.
+  void set_prologue(uint64_t ticket, void* producer_stream, std::vector<lzk_copy_desc> inline_descs,
+                    std::vector<std::shared_ptr<DeviceRegion>> inline_regions);
   bool ticket_complete(uint64_t ticket) const;
   // Device time of a completed ticket's snapshot (CUDA events on the snapshot
   // stream, first device op -> last completion); < 0 when not measured.
@@ -221,6 +232,13 @@ class TransferEngine {
     uint32_t kernel_ctas = 0;    // gather grid for this group
     lzk_event* done = nullptr;   // recorded after the group's device work
     bool issue_failed = false;
+    bool host_after_device = false;  // host copies read bytes the prologue writes
+  };
+  struct InlineWatch {
+    std::shared_ptr<DeviceRegion> region;
+    uint64_t captured = 0;
+    uint64_t fence = 0;
+    bool fenced = false;
   };
   struct TicketProgress {
     uint64_t expected = 0;
@@ -232,6 +250,11 @@ class TransferEngine {
     lzk_event* start_event = nullptr;  // recorded before the ticket's first group
     double device_ms = -1;             // first issue -> last completion, on the device
     std::vector<std::shared_ptr<CopyTask>> tasks;  // for fence versions
+    // set_prologue: consumed by the issuer before the ticket's first group
+    lzk_event* producer = nullptr;
+    std::vector<lzk_copy_desc> inline_descs;
+    bool prologue = false;                 // the ticket's __meta__ is written on the device
+    std::vector<InlineWatch> inline_watch;  // verdict at the first completed group
   };
 
   void issuer_loop();

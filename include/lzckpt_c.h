@@ -10,6 +10,7 @@
  *   lzckpt_plan_shards       plan_checkpoint         topology.hpp:97-98
  *   lzckpt_engine_create     Engine::Engine          engine.hpp:88
  *   lzckpt_engine_capture    Engine::capture         engine.hpp:97-98 / engine.cpp:96-231
+ *   lzckpt_engine_capture_on_stream  Engine::capture, ordered after a trainer stream
  *   lzckpt_engine_update_barrier
  *                            Engine::update_barrier  engine.hpp:103 / engine.cpp:233-253
  *   lzckpt_engine_wait_persisted, _drain, _restore, _counters
@@ -207,6 +208,14 @@ void lzckpt_engine_destroy(lzckpt_engine* e);
 /* plan = plan_checkpoint(engine topology, *model, step) */
 int lzckpt_engine_capture(lzckpt_engine* e, const lzckpt_model_spec* model, const lzckpt_tree* t,
                           uint64_t step, lzckpt_ticket** out);
+/* Engine::capture(plan, tree, step, producer_stream): the same capture,
+ * ordered on the device after the work already queued on the trainer's
+ * `cuda_stream` (a cudaStream_t; NULL = the legacy default stream), so the
+ * snapshot never reads a tensor the trainer is still writing. The host does
+ * not wait; inline leaves are read behind the producer too. The reference
+ * orders reads after writes with its region mutex (transfer_engine.cpp:10-36). */
+int lzckpt_engine_capture_on_stream(lzckpt_engine* e, const lzckpt_model_spec* model, const lzckpt_tree* t,
+                                    uint64_t step, void* cuda_stream, lzckpt_ticket** out);
 int lzckpt_engine_update_barrier(lzckpt_engine* e, lzckpt_ticket* k);
 int lzckpt_engine_update_barrier_on_stream(lzckpt_engine* e, lzckpt_ticket* k, void* cuda_stream);
 int lzckpt_engine_wait_persisted(lzckpt_engine* e, lzckpt_ticket* k);
@@ -260,6 +269,8 @@ int lzckpt_engine_flush_stats(const lzckpt_engine* e, uint64_t* bytes_written, u
  * every leaf of the tree, same lazy snapshot path, no plan. */
 int lzckpt_engine_capture_file(lzckpt_engine* e, const char* path, const lzckpt_tree* t, uint64_t step,
                                lzckpt_ticket** out);
+int lzckpt_engine_capture_file_on_stream(lzckpt_engine* e, const char* path, const lzckpt_tree* t, uint64_t step,
+                                         void* cuda_stream, lzckpt_ticket** out);
 /* Reads one file back (validated). Region leaves are DMA'd into the
  * same-path, same-size regions of `into` (may be NULL), else fresh regions. */
 int lzckpt_engine_restore_file(lzckpt_engine* e, const char* path, const lzckpt_tree* into, lzckpt_tree** out);

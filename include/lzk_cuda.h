@@ -105,8 +105,9 @@ int lzk_host_register(void* ptr, uint64_t bytes);
 int lzk_host_unregister(void* ptr);
 
 /* ---- streams and events ------------------------------------------------ */
-/* priority: 0 = default; >0 = lower priority than compute (snapshot work
- * yields SMs to training kernels); <0 = higher. */
+/* priority: <0 = the greatest priority; 0 and >0 = the least, which on
+ * current GPUs is also the default (CUDA has nothing below an ordinary
+ * stream). */
 int lzk_stream_create(int device, int priority, lzk_stream** s);
 /* Wraps a foreign cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)
  * without taking ownership. */
@@ -125,6 +126,13 @@ int lzk_event_sync(lzk_event* e);
 int lzk_event_elapsed_ms(lzk_event* start, lzk_event* end, float* ms);
 /* Device-side fence: work queued on `s` after this call waits for `e`. */
 int lzk_stream_wait_event(lzk_stream* s, lzk_event* e);
+/* Records `e` on a raw cudaStream_t owned by the caller (NULL = the legacy
+ * default stream): how capture() marks "everything the trainer has queued so
+ * far" on the producer stream before the snapshot stream waits for it. */
+int lzk_event_record_raw(lzk_event* e, void* cuda_stream);
+/* `s` waits for the work queued so far on a raw producer stream (NULL = the
+ * legacy default stream). */
+int lzk_stream_wait_raw(lzk_stream* s, void* producer_stream);
 /* Same, for a raw cudaStream_t handle owned by the caller. */
 int lzk_raw_stream_wait_event(void* cuda_stream, lzk_event* e);
 

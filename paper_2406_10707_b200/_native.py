@@ -134,6 +134,7 @@ ENGINE_SYMBOLS = [
     ("lzckpt_engine_create", i32, [P(EngineConfigC), P(Topology), u32, u32, u32, P(vp)]),
     ("lzckpt_engine_destroy", None, [vp]),
     ("lzckpt_engine_capture", i32, [vp, P(ModelSpecC), vp, u64, P(vp)]),
+    ("lzckpt_engine_capture_on_stream", i32, [vp, P(ModelSpecC), vp, u64, vp, P(vp)]),
     ("lzckpt_engine_update_barrier", i32, [vp, vp]),
     ("lzckpt_engine_update_barrier_on_stream", i32, [vp, vp, vp]),
     ("lzckpt_engine_wait_persisted", i32, [vp, vp]),
@@ -146,6 +147,7 @@ ENGINE_SYMBOLS = [
     ("lzckpt_engine_snapshot_stream", vp, [vp]),
     ("lzckpt_engine_set_copy_variant", i32, [vp, u64, i32, i32, u32, u64]),
     ("lzckpt_engine_capture_file", i32, [vp, cp, vp, u64, P(vp)]),
+    ("lzckpt_engine_capture_file_on_stream", i32, [vp, cp, vp, u64, vp, P(vp)]),
     ("lzckpt_engine_commit", i32, [vp, P(ModelSpecC), vp, vp, P(i32), cp, u64]),
     ("lzckpt_file_digest", i32, [cp, i32, P(u64), P(u64)]),
     ("lzckpt_trim_caches", None, []),
@@ -195,6 +197,8 @@ DEVICE_SYMBOLS = [
     ("lzk_event_elapsed_ms", i32, [vp, vp, P(C.c_float)]),
     ("lzk_stream_wait_event", i32, [vp, vp]),
     ("lzk_raw_stream_wait_event", i32, [vp, vp]),
+    ("lzk_event_record_raw", i32, [vp, vp]),
+    ("lzk_stream_wait_raw", i32, [vp, vp]),
     ("lzk_gather_d2h", i32, [vp, P(CopyDescC), u32, u32]),
     ("lzk_ce_copy_d2h", i32, [vp, P(CopyDescC), u32]),
     ("lzk_scatter_h2d", i32, [vp, P(CopyDescC), u32, u32]),

@@ -66,12 +66,18 @@ class DataStatesCheckpointEngine:
     def makedirs(self, path, exist_ok: bool = False) -> None:
         os.makedirs(path, exist_ok=exist_ok)
 
-    def save(self, state_dict: Any, path: str) -> None:
+    def save(self, state_dict: Any, path: str, stream=None) -> None:
+        """Queues the snapshot and returns. It is ordered on the device after
+        the work already queued on `stream` (default: the current torch stream),
+        so a save right after an un-synchronised optimizer.step() reads the
+        updated tensors, never half-written ones."""
+        import torch
         tree = L.StateTree()
         skeleton = self._flatten(state_dict, "s", tree)
         tree.set_blob(SKELETON, pickle.dumps(skeleton, protocol=pickle.HIGHEST_PROTOCOL))
         self._step += 1
-        self._pending.append(self._engine.capture_file(path, tree, self._step))
+        producer = torch.cuda.current_stream(self.device) if stream is None else stream
+        self._pending.append(self._engine.capture_file(path, tree, self._step, producer_stream=producer))
         self._keep.append(tree)
 
     def wait(self, stream=None) -> None:

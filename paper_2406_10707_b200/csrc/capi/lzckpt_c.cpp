@@ -530,6 +530,18 @@ int lzckpt_engine_capture(lzckpt_engine* e, const lzckpt_model_spec* model, cons
   });
 }
 
+int lzckpt_engine_capture_on_stream(lzckpt_engine* e, const lzckpt_model_spec* model, const lzckpt_tree* t,
+                                    uint64_t step, void* cuda_stream, lzckpt_ticket** out) {
+  return guard([&] {
+    need(e, "engine");
+    need(model, "model");
+    need(t, "tree");
+    need(out, "out");
+    CheckpointPlan plan = plan_checkpoint(e->topo, to_model(model), step);
+    *out = new lzckpt_ticket{e->e->capture(plan, t->t, step, cuda_stream)};
+  });
+}
+
 int lzckpt_engine_update_barrier(lzckpt_engine* e, lzckpt_ticket* k) {
   return guard([&] {
     need(e, "engine");
@@ -676,6 +688,17 @@ int lzckpt_engine_capture_file(lzckpt_engine* e, const char* path, const lzckpt_
     need(t, "tree");
     need(out, "out");
     *out = new lzckpt_ticket{e->e->capture_file(path, t->t, step)};
+  });
+}
+
+int lzckpt_engine_capture_file_on_stream(lzckpt_engine* e, const char* path, const lzckpt_tree* t, uint64_t step,
+                                         void* cuda_stream, lzckpt_ticket** out) {
+  return guard([&] {
+    need(e, "engine");
+    need(path, "path");
+    need(t, "tree");
+    need(out, "out");
+    *out = new lzckpt_ticket{e->e->capture_file(path, t->t, step, cuda_stream)};
   });
 }
 

@@ -653,6 +653,25 @@ int lzk_stream_wait_event(lzk_stream* s, lzk_event* e) {
   return LZK_OK;
 }
 
+int lzk_event_record_raw(lzk_event* e, void* cuda_stream) {
+  if (!e) return fail(LZK_ERR_INVALID, "null event");
+  if (int rc = use_device(e->device)) return rc;
+  LZK_CK(cudaEventRecord(e->e, static_cast<cudaStream_t>(cuda_stream)));
+  return LZK_OK;
+}
+
+int lzk_stream_wait_raw(lzk_stream* s, void* producer_stream) {
+  if (!s) return fail(LZK_ERR_INVALID, "null stream");
+  if (int rc = use_device(s->device)) return rc;
+  cudaEvent_t e = nullptr;
+  LZK_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaError_t r = cudaEventRecord(e, static_cast<cudaStream_t>(producer_stream));
+  if (r == cudaSuccess) r = cudaStreamWaitEvent(s->s, e, 0);
+  cudaEventDestroy(e);  // released once the queued wait has fired
+  if (r != cudaSuccess) return cuda_fail(r, "lzk_stream_wait_raw");
+  return LZK_OK;
+}
+
 int lzk_raw_stream_wait_event(void* cuda_stream, lzk_event* e) {
   if (!e) return fail(LZK_ERR_INVALID, "null event");
   LZK_CK(cudaStreamWaitEvent(static_cast<cudaStream_t>(cuda_stream), e->e, 0));

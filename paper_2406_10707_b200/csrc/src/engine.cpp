@@ -213,9 +213,8 @@ std::shared_ptr<const std::byte> Engine::meta_buffer(uint64_t bytes) {
   });
 }
 
-std::shared_ptr<CaptureTicket> Engine::capture(const CheckpointPlan& plan, const StateTree& state,
-                                               uint64_t step) {
-  const auto t0 = std::chrono::steady_clock::now();
+std::vector<Engine::FileSpec> Engine::plan_files(const CheckpointPlan& plan, const StateTree& state,
+                                                 uint64_t step) const {
   PhaseTrace ftr("capture-flatten");
   const auto& shards = plan.shards(flat_rank(topo_, rank_));
   const auto names = state.top_level_names();
@@ -239,24 +238,53 @@ std::shared_ptr<CaptureTicket> Engine::capture(const CheckpointPlan& plan, const
     }
   }
   ftr.mark("flatten");
-  return capture_impl(files, step, t0);
+  return files;
 }
+
+std::shared_ptr<CaptureTicket> Engine::capture(const CheckpointPlan& plan, const StateTree& state,
+                                               uint64_t step) {
+  const auto t0 = std::chrono::steady_clock::now();
+  auto files = plan_files(plan, state, step);
+  return capture_impl(files, step, t0, Producer{});
+}
+
+std::shared_ptr<CaptureTicket> Engine::capture(const CheckpointPlan& plan, const StateTree& state,
+                                               uint64_t step, void* producer_stream) {
+  const auto t0 = std::chrono::steady_clock::now();
+  auto files = plan_files(plan, state, step);
+  return capture_impl(files, step, t0, Producer{true, producer_stream});
+}
+
+namespace {
+
+std::vector<StateTree::FlatLeaf> file_leaves(const StateTree& state) {
+  auto leaves = state.flatten();
+  if (leaves.empty()) throw ConfigError("capture_file: empty state tree");
+  return leaves;
+}
+
+}  // namespace
 
 std::shared_ptr<CaptureTicket> Engine::capture_file(const std::filesystem::path& path, const StateTree& state,
                                                     uint64_t step) {
   const auto t0 = std::chrono::steady_clock::now();
   std::vector<FileSpec> files(1);
   files[0].path = path;
-  files[0].leaves = std::make_shared<const std::vector<StateTree::FlatLeaf>>(state.flatten());
-  uint64_t sum = 0;
-  for (const auto& l : *files[0].leaves) sum += l.size;
-  if (files[0].leaves->empty()) throw ConfigError("capture_file: empty state tree");
-  (void)sum;
-  return capture_impl(files, step, t0);
+  files[0].leaves = std::make_shared<const std::vector<StateTree::FlatLeaf>>(file_leaves(state));
+  return capture_impl(files, step, t0, Producer{});
+}
+
+std::shared_ptr<CaptureTicket> Engine::capture_file(const std::filesystem::path& path, const StateTree& state,
+                                                    uint64_t step, void* producer_stream) {
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<FileSpec> files(1);
+  files[0].path = path;
+  files[0].leaves = std::make_shared<const std::vector<StateTree::FlatLeaf>>(file_leaves(state));
+  return capture_impl(files, step, t0, Producer{true, producer_stream});
 }
 
 std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files, uint64_t step,
-                                                    std::chrono::steady_clock::time_point t0) {
+                                                    std::chrono::steady_clock::time_point t0, Producer producer) {
   detail::NvtxRange range("lzckpt.capture");
   PhaseTrace tr;
   std::vector<ShardBuild> builds(files.size());
@@ -273,12 +301,18 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
   }
   tr.mark("flatten+validate");
 
+  // Ordered capture on the device path: the inline gather becomes the
+  // ticket's first device op (after the producer wait) instead of a
+  // synchronous launch here. The paced channel is host-driven, so there the
+  // inline gather stays synchronous, behind a device-side producer wait.
+  const bool deferred_inline = producer.ordered && config_.copy_channel.bandwidth_Bps <= 0;
+  std::vector<lzk_copy_desc> inl;
+  std::vector<StateTree::RegionPtr> inl_regions;
   {
     std::lock_guard il(inline_mu_);  // one inline gather at a time (inline_stream_)
     // Small region leaves go straight from HBM into their slots of __meta__
     // (pinned, mapped), by ONE gather launch for the whole capture; the
     // reference clones each under a lock (engine.cpp:138-143).
-    std::vector<lzk_copy_desc> inl;
     for (size_t i = 0; i < files.size(); ++i) {
       ShardBuild& b = builds[i];
       b.shard_id = files[i].shard_id;
@@ -315,6 +349,7 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
           if (l.region) {
             if (l.size) {
               inl.push_back({reinterpret_cast<uint64_t>(l.region->device_ptr()), reinterpret_cast<uint64_t>(p), l.size});
+              if (deferred_inline) inl_regions.push_back(l.region);
             }
           } else if (l.size) {
             std::memcpy(p, l.blob->data(), l.size);
@@ -333,8 +368,9 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
       b.payload = cursor - b.header.serialized_size();
     }
     tr.mark("meta+header");
-    if (!inl.empty()) {
+    if (!inl.empty() && !deferred_inline) {
       // synchronous: the bytes are captured before capture() returns
+      if (producer.ordered) ck(lzk_stream_wait_raw(inline_stream_, producer.stream), "inline gather: producer wait");
       ck(lzk_gather_d2h(inline_stream_, inl.data(), uint32_t(inl.size()), config_.snapshot.kernel_ctas),
          "inline leaf gather");
       ck(lzk_stream_sync(inline_stream_), "inline leaf gather sync");
@@ -351,6 +387,13 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
     ticket->engine_ = this;
     std::erase_if(tickets_, [](const auto& kv) { return kv.second.expired(); });
     tickets_.emplace(ticket->id_, ticket);
+  }
+  if (deferred_inline) {
+    transfers_.set_prologue(ticket->id_, producer.stream, std::move(inl), std::move(inl_regions));
+  } else if (producer.ordered) {
+    // paced channel: its host-driven reads are ordered by a host wait here
+    ck(lzk_stream_wait_raw(inline_stream_, producer.stream), "capture: producer wait");
+    ck(lzk_stream_sync(inline_stream_), "capture: producer wait");
   }
 
   uint64_t total = 0;

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <utility>
 
 #include "lzckpt/errors.hpp"
 #include "lzk_cuda.h"
@@ -236,6 +237,29 @@ void TransferEngine::submit_copies(uint64_t ticket, std::vector<std::shared_ptr<
   bytes_submitted_.fetch_add(added);
 }
 
+void TransferEngine::set_prologue(uint64_t ticket, void* producer_stream, std::vector<lzk_copy_desc> inline_descs,
+                                  std::vector<std::shared_ptr<DeviceRegion>> inline_regions) {
+  if (channel_.bandwidth_Bps > 0) throw Error("set_prologue: the paced channel is host-driven");
+  lzk_event* e = take_event();
+  if (int rc = lzk_event_record_raw(e, producer_stream); rc != LZK_OK) {
+    std::lock_guard lk(mu_);
+    give_event(e);
+    ck(rc, "set_prologue: record on the producer stream");
+  }
+  std::lock_guard lk(mu_);
+  auto& tp = tickets_[ticket];
+  if (tp.producer) give_event(tp.producer);
+  tp.producer = e;
+  tp.inline_descs = std::move(inline_descs);
+  tp.prologue = true;
+  tp.inline_watch.clear();
+  tp.inline_watch.reserve(inline_regions.size());
+  for (auto& r : inline_regions) {
+    const uint64_t v = r->version();
+    tp.inline_watch.push_back(InlineWatch{std::move(r), v, 0, false});
+  }
+}
+
 // Cuts tasks into quantum-sized pieces (the reference's chunk grid, which
 // fixes the announcement sequence) and packs pieces into groups of about
 // group_bytes; each region piece becomes a gather-kernel or copy-engine
@@ -312,9 +336,23 @@ void TransferEngine::issuer_loop() {
       issuing_ = true;
     }
     lzk_event* start = nullptr;
+    lzk_event* producer = nullptr;
+    std::vector<lzk_copy_desc> inl;
     {
       std::lock_guard lk(mu_);
-      if (!tickets_[g.ticket].start_event) start = reinterpret_cast<lzk_event*>(1);
+      auto& tp = tickets_[g.ticket];
+      if (!tp.start_event) start = reinterpret_cast<lzk_event*>(1);
+      producer = std::exchange(tp.producer, nullptr);
+      if (producer) inl = std::move(tp.inline_descs);
+      g.host_after_device = tp.prologue;
+    }
+    bool pre_ok = true;
+    if (producer) {
+      // the ticket's first device op: wait for what the trainer queued
+      // before capture(); the event can be recycled once the wait is queued
+      pre_ok = lzk_stream_wait_event(stream_, producer) == LZK_OK;
+      std::lock_guard lk(mu_);
+      give_event(producer);
     }
     if (start) {
       start = take_event();
@@ -324,7 +362,14 @@ void TransferEngine::issuer_loop() {
         start = nullptr;
       }
     }
+    if (pre_ok && !inl.empty()) {
+      pre_ok = lzk_gather_d2h(stream_, inl.data(), uint32_t(inl.size()), g.kernel_ctas) == LZK_OK;
+      std::lock_guard lk(mu_);
+      stats_.kernel_launches += (inl.size() + 959) / 960;
+      for (const auto& d : inl) stats_.kernel_bytes += d.len;
+    }
     issue(g);
+    g.issue_failed = g.issue_failed || !pre_ok;
     {
       std::lock_guard lk(mu_);
       issuing_ = false;
@@ -400,21 +445,39 @@ static bool torn_verdict(const CopyTask& t) {
 
 void TransferEngine::run_device_group(Group& g) {
   // Host blobs (the __meta__ entry, large host leaves) are host->pinned
-  // memcpys; do them while the device copies are in flight.
+  // memcpys; do them while the device copies are in flight — or after them
+  // when a capture prologue writes inline leaves into __meta__ on the device.
   uint64_t blob = 0;
-  for (const auto& p : g.pieces) {
-    const CopyTask& t = *p.task;
-    if (!t.source.is_host()) continue;
-    const Segment seg = pool_.segment_info(t.segment_id);
-    std::memcpy(pool_.segment_data(seg) + t.dst_offset + p.offset,
-                t.source.host_data() + t.src_offset + p.offset, p.length);
-    blob += p.length;
-  }
+  auto host_copies = [&] {
+    for (const auto& p : g.pieces) {
+      const CopyTask& t = *p.task;
+      if (!t.source.is_host()) continue;
+      const Segment seg = pool_.segment_info(t.segment_id);
+      std::memcpy(pool_.segment_data(seg) + t.dst_offset + p.offset,
+                  t.source.host_data() + t.src_offset + p.offset, p.length);
+      blob += p.length;
+    }
+  };
+  if (!g.host_after_device) host_copies();
   const bool device_ok = !g.issue_failed && lzk_event_sync(g.done) == LZK_OK;
+  if (g.host_after_device) host_copies();
   std::vector<char> torn(g.pieces.size(), 0);
+  bool inline_torn = false;
   {
     std::lock_guard lk(mu_);
     stats_.blob_bytes += blob;
+    // The prologue's inline gather ran before this group on the stream: its
+    // verdict is due at the ticket's first completed group.
+    auto& tp = tickets_[g.ticket];
+    if (!tp.inline_watch.empty()) {
+      for (const auto& w : tp.inline_watch) {
+        const uint64_t seen = w.fenced ? w.fence : w.region->version();
+        inline_torn = inline_torn || seen != w.captured;
+      }
+      inline_torn = inline_torn || !device_ok;
+      tp.inline_watch.clear();
+      if (inline_torn) tp.torn = true;
+    }
     for (size_t i = 0; i < g.pieces.size(); ++i) {
       const Piece& p = g.pieces[i];
       if (!p.last) continue;
@@ -423,6 +486,11 @@ void TransferEngine::run_device_group(Group& g) {
       torn[i] = !device_ok || torn_verdict(*p.task);
       p.task->state.store(torn[i] ? CopyState::Torn : CopyState::Done);
     }
+  }
+  if (inline_torn && torn_cb_) {
+    CopyTask marker;  // the torn callback needs only the ticket
+    marker.ticket = g.ticket;
+    torn_cb_(marker);
   }
   std::vector<ChunkSpan> spans;
   uint64_t delivered = 0;
@@ -545,6 +613,10 @@ bool TransferEngine::fence_on_stream(uint64_t ticket, void* cuda_stream) {
     if (s == CopyState::Done || s == CopyState::Torn || !t->source.region) continue;
     t->fence_version = t->source.region->version();
     t->fenced = true;
+  }
+  for (auto& w : tp.inline_watch) {
+    w.fence = w.region->version();
+    w.fenced = true;
   }
   if (tp.last_event) ck(lzk_raw_stream_wait_event(cuda_stream, tp.last_event), "fence_on_stream");
   return true;

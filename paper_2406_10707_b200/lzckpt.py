@@ -11,6 +11,7 @@ from __future__ import annotations
 import ctypes as C
 import dataclasses
 import os
+import sys
 from typing import Callable, Iterable, List, Optional, Sequence, Tuple
 
 from . import _native as N
@@ -620,6 +621,35 @@ class Counters:
     last_barrier_seconds: float
 
 
+class _CurrentStream:
+    """Default producer for Engine.capture: torch's current CUDA stream on the
+    engine's device (when torch has initialised CUDA in this process)."""
+
+    def __repr__(self):
+        return "CURRENT_STREAM"
+
+
+CURRENT_STREAM = _CurrentStream()
+
+
+def _producer(stream, device: int):
+    """(ordered, cudaStream_t) for a capture's producer argument.
+
+    CURRENT_STREAM -> torch.cuda.current_stream(device) if torch has set up
+    CUDA here, else unordered (no torch work can be pending); None ->
+    unordered, the reference call; a torch.cuda.Stream or a raw int handle
+    (0 = the legacy default stream) -> ordered after that stream."""
+    if stream is CURRENT_STREAM:
+        torch = sys.modules.get("torch")
+        if torch is None or not torch.cuda.is_initialized():
+            return False, None
+        d = torch.cuda.current_device() if device < 0 else device
+        return True, torch.cuda.current_stream(d).cuda_stream
+    if stream is None:
+        return False, None
+    return True, int(getattr(stream, "cuda_stream", stream))
+
+
 class Engine:
     def __init__(self, config: EngineConfig, topo: ParallelTopology, rank: RankCoord):
         self.config, self.topo, self.rank = config, topo, rank
@@ -641,9 +671,20 @@ class Engine:
     def __exit__(self, *a):
         self.close()
 
-    def capture(self, plan: CheckpointPlan, state: StateTree, step: int) -> CaptureTicket:
+    def capture(self, plan: CheckpointPlan, state: StateTree, step: int,
+                producer_stream=CURRENT_STREAM) -> CaptureTicket:
+        """Engine::capture. The snapshot is ordered on the device after the work
+        already queued on `producer_stream` (default: torch's current stream),
+        so it never reads a tensor the trainer is still writing; the host does
+        not wait. producer_stream=None is the reference call (inline leaves
+        cloned synchronously, no producer ordering)."""
         h = C.c_void_p()
-        _check(lib.lzckpt_engine_capture(self._h, C.byref(plan.model._c()), state._h, step, C.byref(h)))
+        ordered, handle = _producer(producer_stream, self.config.device)
+        if ordered:
+            _check(lib.lzckpt_engine_capture_on_stream(self._h, C.byref(plan.model._c()), state._h, step, handle,
+                                                       C.byref(h)))
+        else:
+            _check(lib.lzckpt_engine_capture(self._h, C.byref(plan.model._c()), state._h, step, C.byref(h)))
         return CaptureTicket(h)
 
     def ticket_headers(self, t: CaptureTicket) -> List[CheckpointFileHeader]:
@@ -654,9 +695,14 @@ class Engine:
             out.append(_from_handle(hh))
         return out
 
-    def capture_file(self, path, state: StateTree, step: int) -> CaptureTicket:
+    def capture_file(self, path, state: StateTree, step: int, producer_stream=CURRENT_STREAM) -> CaptureTicket:
         h = C.c_void_p()
-        _check(lib.lzckpt_engine_capture_file(self._h, os.fspath(path).encode(), state._h, step, C.byref(h)))
+        ordered, handle = _producer(producer_stream, self.config.device)
+        if ordered:
+            _check(lib.lzckpt_engine_capture_file_on_stream(self._h, os.fspath(path).encode(), state._h, step,
+                                                            handle, C.byref(h)))
+        else:
+            _check(lib.lzckpt_engine_capture_file(self._h, os.fspath(path).encode(), state._h, step, C.byref(h)))
         return CaptureTicket(h)
 
     def restore_file(self, path, into: Optional[StateTree] = None) -> StateTree:
