@@ -233,6 +233,16 @@ int lzckpt_engine_commit(lzckpt_engine* e, const lzckpt_model_spec* model, lzckp
 /* Restore/commit keep their pinned + device stream windows (3 x 512 MiB each)
  * pooled for the next call; this frees the idle ones. */
 void lzckpt_trim_caches(void);
+/* NUMA placement. Each engine places its pinned ring on
+ * its GPU's NUMA node (MPOL_PREFERRED before first touch, by that node's
+ * CPUs) and binds its issuer, completion, flush and streamer threads there;
+ * lzckpt_engine_numa_node reports the node (-1 = none: single-node host).
+ * The helpers below expose the same policy for tests and tools. */
+int lzckpt_numa_node_count(void);
+int lzckpt_numa_prefer_range(void* p, uint64_t len, int node);
+/* Node of each page at p + k*stride (move_pages query), k < cap; *n = pages. */
+int lzckpt_numa_page_nodes(const void* p, uint64_t len, uint64_t stride, int* nodes, uint64_t cap, uint64_t* n);
+int lzckpt_engine_numa_node(const lzckpt_engine* e);
 /* Phase one of the 2PC for THIS rank only (EngineCommitParticipant::prepare,
  * reference consolidation.cpp:142-152): waits until the capture is persisted,
  * then validates the rank's files on the GPU. Writes a JSON vote

@@ -99,6 +99,12 @@ int lzk_memcpy_d2d(int device, void* dst, const void* src, uint64_t bytes);
 #define LZK_HOST_MAPPED 0x1    /* device-visible alias (UVA: same address) */
 #define LZK_HOST_HUGEPAGE 0x2  /* mmap + MADV_HUGEPAGE + parallel first touch + register */
 int lzk_host_alloc(uint64_t bytes, int flags, void** ptr);
+/* Same, with the pages placed on `numa_node` (MPOL_PREFERRED set before the
+ * first touch, which that node's CPUs perform); -1 = no placement. */
+int lzk_host_alloc_numa(uint64_t bytes, int flags, int numa_node, void** ptr);
+/* NUMA node of the GPU's PCI function (/sys/bus/pci/devices/<bdf>/numa_node);
+ * -1 when the host does not report one (single-node machines). */
+int lzk_device_numa_node(int device, int* node);
 int lzk_host_free(void* ptr);
 /* Pins an existing host range (e.g. a numpy buffer) for direct DMA. */
 int lzk_host_register(void* ptr, uint64_t bytes);

@@ -151,6 +151,10 @@ ENGINE_SYMBOLS = [
     ("lzckpt_engine_commit", i32, [vp, P(ModelSpecC), vp, vp, P(i32), cp, u64]),
     ("lzckpt_file_digest", i32, [cp, i32, P(u64), P(u64)]),
     ("lzckpt_trim_caches", None, []),
+    ("lzckpt_numa_node_count", i32, []),
+    ("lzckpt_numa_prefer_range", i32, [vp, u64, i32]),
+    ("lzckpt_numa_page_nodes", i32, [vp, u64, u64, P(i32), u64, P(u64)]),
+    ("lzckpt_engine_numa_node", i32, [vp]),
     ("lzckpt_engine_prepare", i32, [vp, P(ModelSpecC), vp, cp, u64, P(u64)]),
     ("lzckpt_engine_ticket_header", i32, [vp, vp, u32, P(vp)]),
     ("lzckpt_engine_restore_file", i32, [vp, cp, vp, P(vp)]),
@@ -180,6 +184,8 @@ DEVICE_SYMBOLS = [
     ("lzk_memcpy_d2h", i32, [i32, vp, vp, u64]),
     ("lzk_memcpy_d2d", i32, [i32, vp, vp, u64]),
     ("lzk_host_alloc", i32, [u64, i32, P(vp)]),
+    ("lzk_host_alloc_numa", i32, [u64, i32, i32, P(vp)]),
+    ("lzk_device_numa_node", i32, [i32, P(i32)]),
     ("lzk_host_free", i32, [vp]),
     ("lzk_host_register", i32, [vp, u64]),
     ("lzk_host_unregister", i32, [vp]),

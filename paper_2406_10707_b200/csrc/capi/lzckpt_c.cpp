@@ -12,6 +12,7 @@
 #include <json.hpp>
 #include "lzckpt/engine.hpp"
 #include "lzckpt/errors.hpp"
+#include "../src/numa.hpp"
 #include "lzckpt/format.hpp"
 #include "lzckpt/manifest.hpp"
 #include "lzckpt/ring_core.hpp"
@@ -601,6 +602,27 @@ int lzckpt_file_digest(const char* path, int device, uint64_t* length, uint64_t*
 }
 
 void lzckpt_trim_caches(void) { detail::FileStreamer::trim(); }
+
+int lzckpt_numa_node_count(void) { return detail::numa_node_count(); }
+
+int lzckpt_numa_prefer_range(void* p, uint64_t len, int node) {
+  return guard([&] {
+    need(p, "range");
+    if (!detail::prefer_node(p, len, node)) throw Error("mbind(MPOL_PREFERRED) failed");
+  });
+}
+
+int lzckpt_numa_page_nodes(const void* p, uint64_t len, uint64_t stride, int* nodes, uint64_t cap, uint64_t* n) {
+  return guard([&] {
+    need(p, "range");
+    need(nodes, "nodes");
+    const int r = detail::page_nodes(p, len, stride, nodes, cap);
+    if (r < 0) throw Error("move_pages query failed: errno " + std::to_string(-r));
+    if (n) *n = uint64_t(r);
+  });
+}
+
+int lzckpt_engine_numa_node(const lzckpt_engine* e) { return e ? e->e->pool().numa_node() : -1; }
 
 int lzckpt_engine_prepare(lzckpt_engine* e, const lzckpt_model_spec* model, lzckpt_ticket* t, char* json,
                           uint64_t cap, uint64_t* needed) {

@@ -30,6 +30,7 @@
 #include "file_stream.hpp"
 #include "lzckpt/errors.hpp"
 #include "lzk_cuda.h"
+#include "numa.hpp"
 
 namespace lzckpt {
 
@@ -129,7 +130,12 @@ Engine::Engine(EngineConfig config, ParallelTopology topo, RankCoord rank)
     : config_(std::move(config)),
       topo_(topo),
       rank_(rank),
-      pool_(config_.host_buffer_bytes, config_.reserve_timeout, config_.pool),
+      pool_(config_.host_buffer_bytes, config_.reserve_timeout,
+            [this] {
+              PoolOptions o = config_.pool;
+              if (o.device < 0) o.device = config_.snapshot.device;
+              return o;
+            }()),
       transfers_(pool_, config_.copy_channel, config_.snapshot),
       flush_(pool_, config_.flush) {
   topo_.validate();
@@ -542,6 +548,7 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
 // on pool backpressure, i.e. on the flush draining earlier segments),
 // attaches it to its file and submits its copies.
 void Engine::streamer_loop() {
+  detail::bind_thread_to_node(pool_.numa_node());
   for (;;) {
     StreamJob j;
     {

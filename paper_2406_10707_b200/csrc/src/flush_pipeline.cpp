@@ -26,6 +26,7 @@
 
 #include "lzckpt/errors.hpp"
 #include "lzk_cuda.h"
+#include "numa.hpp"
 
 namespace lzckpt {
 
@@ -375,6 +376,7 @@ size_t FlushPipeline::queue_depth() const {
 }
 
 void FlushPipeline::worker_loop() {
+  detail::bind_thread_to_node(pool_.numa_node());  // hashes and writes the ring's bytes
   std::unique_lock lk(mu_);
   for (;;) {
     work_cv_.wait(lk, [&] { return stopping_ || !jobs_.empty(); });

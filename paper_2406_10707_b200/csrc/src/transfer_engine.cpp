@@ -15,6 +15,7 @@
 
 #include "lzckpt/errors.hpp"
 #include "lzk_cuda.h"
+#include "numa.hpp"
 
 namespace lzckpt {
 
@@ -321,6 +322,7 @@ void TransferEngine::issue(Group& g) {
 }
 
 void TransferEngine::issuer_loop() {
+  detail::bind_thread_to_node(pool_.numa_node());
   for (;;) {
     Group g;
     {
@@ -392,6 +394,7 @@ void TransferEngine::issuer_loop() {
 }
 
 void TransferEngine::worker_loop() {
+  detail::bind_thread_to_node(pool_.numa_node());  // it memcpys __meta__ into the ring
   for (;;) {
     Group g;
     {

@@ -741,6 +741,10 @@ class Engine:
         _check(lib.lzckpt_engine_commit(self._h, C.byref(model._c()), t._h, manifest._h, C.byref(ok), reason, 1024))
         return bool(ok.value), reason.value.decode(errors="replace")
 
+    def numa_node(self) -> int:
+        """NUMA node of this engine's pinned ring and threads (-1: none)."""
+        return lib.lzckpt_engine_numa_node(self._h)
+
     def counters(self) -> Counters:
         c = N.CountersC()
         _check(lib.lzckpt_engine_counters(self._h, C.byref(c)))
@@ -791,6 +795,30 @@ def trim_caches() -> None:
     """Free the stream windows restore/commit keep pooled between calls
     (3 x 512 MiB pinned + 3 x 512 MiB HBM per device)."""
     lib.lzckpt_trim_caches()
+
+
+def device_numa_node(device: int = 0) -> int:
+    """NUMA node of the GPU's PCI function; -1 when the host reports none."""
+    n = C.c_int(-1)
+    _dev_check(dev.lzk_device_numa_node(device, C.byref(n)))
+    return n.value
+
+
+def numa_node_count() -> int:
+    return lib.lzckpt_numa_node_count()
+
+
+def numa_page_nodes(address: int, length: int, stride: int = 4096) -> List[int]:
+    """Node holding each page of [address, address+length) (move_pages query)."""
+    cap = max(1, (length + stride - 1) // stride)
+    out = (C.c_int * cap)()
+    n = C.c_uint64()
+    _check(lib.lzckpt_numa_page_nodes(address, length, stride, out, cap, C.byref(n)))
+    return list(out[:n.value])
+
+
+def numa_prefer_range(address: int, length: int, node: int) -> None:
+    _check(lib.lzckpt_numa_prefer_range(address, length, node))
 
 
 def device_count() -> int:

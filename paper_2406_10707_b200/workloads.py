@@ -151,11 +151,17 @@ def llama70b_shard(seed: int = 70, layers: int = 10, dp: int = 8, rank: int = 0,
     return w
 
 
-def llama_layer_sample(seed: int = 7, layers: int = 1) -> Workload:
-    """Bounded CPU-baseline sample of C2: `layers` LLaMA-7B decoder layers
-    with the same tensor shapes and 4+12 B/param (3.24 GB per layer)."""
+def llama_layer_sample(seed: int = 7, layers: int = 1, dp: int = 1, rank: int = 0) -> Workload:
+    """Bounded sample of C2 for the reference arm and the matched pair:
+    `layers` LLaMA-7B decoder layers with the C2 tensor shapes and 4+12
+    B/param (3.24 GB per layer). dp > 1: weak scaling, one such shard per rank."""
     tensors = [t for t in _llama7b_tensors(layers=layers) if t[0].startswith("layers.")]
-    return _model_state(f"c2-sample-{layers}l", tensors, 4, layers, "splitmix64", seed)
+    w = _model_state(f"c2-sample-{layers}l", tensors, 4, layers, "splitmix64", seed + rank)
+    if dp > 1:
+        w.param_count *= dp
+        w.topology = (dp, 1, 1, dp, 1)
+        w.rank = (rank, 0, 0)
+    return w
 
 
 def dense_model_shard(name: str, tensors, bpp_model: int, layers: int, seed: int) -> Workload:
