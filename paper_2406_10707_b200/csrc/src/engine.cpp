@@ -865,6 +865,15 @@ void restore_one(const std::filesystem::path& path, StateTree& tree, const State
     }
   }
   tr.mark("regions");
+  bool live = false;  // does the stream write into caller-owned regions?
+  for (const auto& l : leaves) live = live || (!l.inlined && l.is_region && reuse(l));
+  if (live) {
+    // caller-owned regions (e.g. wrapped torch tensors) are written only
+    // after every entry checksum has passed: a corrupt file must leave them
+    // untouched (restore_into's rule)
+    throw_bad(path, streamer.run(path, h, std::vector<EntrySink>(h.entries.size())));
+    tr.mark("validate");
+  }
   throw_bad(path, streamer.run(path, h, sinks));
   tr.mark("stream");
   std::vector<lzk_copy_desc> inl;

@@ -92,6 +92,13 @@ def all_cases():
             ("a", [("r", "w0", 12345), ("r", "w1", None)]),
             ("b", [("r", "m", 500000), ("r", "v", None)]),
         ], 4096, topo=(2, 1, 1, 2, 1), rank=(r, 0, 0), seed=20 + r))
+    # BASELINE configs[2]'s plan shape: dp=8, ranks other than 0 (remainder
+    # bytes go to the low ranks, topology.cpp:151-182)
+    for r in (5, 7):
+        cases.append(_case(f"dp8-rank{r}", 800021, 4, [
+            ("a", [("r", "w0", 3333), ("r", "w1", None)]),
+            ("b", [("r", "m", 400001), ("b", "step", 8), ("r", "v", None)]),
+        ], 4096, topo=(8, 1, 1, 8, 1), rank=(r, 0, 0), seed=70 + r))
     cases.append(_case("pp2tp2-rank3", 400009, 5, [
         ("a", [("r", "w", None)]),
         ("b", [("r", "m", 400000), ("b", "step", 8), ("r", "v", None)]),

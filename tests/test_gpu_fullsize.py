@@ -5,9 +5,10 @@ its flush hashes every entry exactly as for a real file (hash-only tier: C2
 does not fit the box's local disk); the resulting headers - every key,
 offset, length and FNV-1a-64 of every byte - must equal the oracle's
 headers, computed on the CPU from an independent generation of the same
-splitmix64 bytes (oracle.expected_headers). Host memory permitting, the full
-32 layers run; otherwise the largest layer count that fits (stated in the
-assertion message)."""
+splitmix64 bytes (oracle.expected_headers). The full 32 layers must run:
+on a host that cannot pin the 108 GB shard the largest layer count that fits
+is still checked, and the test then XFAILS naming the RAM shortfall, so a
+reduced run can never pass as full size."""
 import os
 import time
 
@@ -55,6 +56,10 @@ def test_c2_fullsize_checksum_of_checksums(lz, oracle, tmp_path):
     print(f"C2 layers={layers}: {t.payload_bytes() / 1e9:.1f} GB, {nentries} entries equal to the oracle "
           f"(oracle {t_oracle:.1f} s, engine capture+hash {t_engine:.1f} s)")
     eng.close()
+    if layers < 32:
+        pytest.xfail(f"host RAM short: MemAvailable {_mem_available() / 1e9:.0f} GB fits {layers} of 32 C2 layers "
+                     f"(needs ~{llama7b_shard().total_bytes * 1.1 / 0.7 / 1e9:.0f} GB); the reduced shard matched")
+    assert t.payload_bytes() > 107e9 and nentries == 906, "full C2 must have run"
 
 
 def test_c4_streamed_70b_shard_checksum_of_checksums(lz, oracle, tmp_path):
@@ -68,7 +73,7 @@ def test_c4_streamed_70b_shard_checksum_of_checksums(lz, oracle, tmp_path):
     w = llama70b_shard()
     pool = 32 << 30
     if pool * 1.5 > _mem_available():
-        pytest.skip("host memory below 48 GiB")
+        pytest.xfail(f"host RAM short: MemAvailable {_mem_available() / 1e9:.0f} GB < 48 GiB for the 32 GiB pool")
     thr = 1 << 20
     expect = oracle.expected_headers(w, thr, threads=os.cpu_count() or 8)
     built = lz.build_workload(w.write_spec(str(tmp_path / "c4.spec")), 0)

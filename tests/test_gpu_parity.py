@@ -676,3 +676,42 @@ def test_restore_and_commit_entries_spanning_windows(gpu, oracle, tmp_path):
     assert n == os.path.getsize(tmp_path / "span.ckpt")
     assert d == oracle.fnv64(np.fromfile(tmp_path / "span.ckpt", dtype=np.uint8))
     eng.close()
+
+
+def test_engine_ring_on_the_gpu_numa_node(gpu, tmp_path):
+    """the pinned ring (and the engine threads) sit on the
+    GPU's NUMA node; on single-node hosts the placement is a no-op (-1)."""
+    lz = gpu
+    eng, _ = small_engine(lz, tmp_path)
+    dev_node = lz.device_numa_node(0)
+    if lz.numa_node_count() < 2 or dev_node < 0:
+        assert eng.numa_node() == -1
+    else:
+        assert eng.numa_node() == dev_node
+    eng.close()
+
+
+def test_restore_file_into_live_regions_validates_first(gpu, tmp_path):
+    """restore_file(path, into): a corrupt file raises ChecksumMismatch and
+    leaves the caller's live regions untouched (every entry is validated
+    before the first byte lands in them, as restore_into does)."""
+    lz = gpu
+    eng, _ = small_engine(lz, tmp_path)
+    tree = lz.StateTree()
+    tree.set_region("x/big", lz.DeviceRegion(bytes(range(256)) * 64))  # 16 KiB: a payload entry
+    tree.set_region("x/small", lz.DeviceRegion(b"abc" * 10))            # inline in __meta__
+    f = tmp_path / "one.lzckpt"
+    t = eng.capture_file(str(f), tree, 1)
+    eng.update_barrier(t)
+    eng.wait_persisted(t)
+    raw = bytearray(f.read_bytes())
+    raw[-5] ^= 0xFF  # inside x/big, the last payload entry
+    f.write_bytes(bytes(raw))
+    live = lz.StateTree()
+    target = lz.DeviceRegion(bytes(16384))
+    live.set_region("x/big", target)
+    live.set_region("x/small", lz.DeviceRegion(bytes(30)))
+    with pytest.raises(lz.ChecksumMismatch):
+        eng.restore_file(str(f), live)
+    assert target.clone_bytes() == bytes(16384)
+    eng.close()
