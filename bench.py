@@ -363,10 +363,9 @@ def main_ours(args, rank, world, local_rank):
             snap(10 + s)
         launches0 = lz.kernel_launches()
         stats0 = eng.snapshot_stats()
-        pcie0 = pcie_tx_bytes(dev)
         dev_ms, host_ms, cap_ms = [], [], []
         barrier()
-        with ClockSampler(dev) as clocks:
+        with ClockSampler(dev) as clocks, PcieSampler(dev) as pcie:
             for s in range(args.steps):
                 barrier()
                 dms, hms, payload, cms = snap(100 + s)
@@ -374,7 +373,6 @@ def main_ours(args, rank, world, local_rank):
                 host_ms.append(hms)
                 cap_ms.append(cms)
             barrier()
-        pcie1 = pcie_tx_bytes(dev)
         launches = lz.kernel_launches() - launches0
         stats1 = eng.snapshot_stats()
         # conservative: the longer of device events and host capture->fence-ready
@@ -437,7 +435,6 @@ def main_ours(args, rank, world, local_rank):
         if rank == 0:
             kernel_gbps = variants["gather_kernel"]
             config = bench_config(world, layers)
-            pcie = pcie1 - pcie0 if pcie0 is not None and pcie1 is not None else None
             line = {
                 "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(statistics.mean(step_ms), 3),
@@ -455,10 +452,10 @@ def main_ours(args, rank, world, local_rank):
                 "roofline": {"bound": "pcie-host-link", "achieved": round(per_gpu, 3), "peak": PCIE_GEN5_X16_GBPS,
                              "unit": "GB/s", "frac": round(per_gpu / PCIE_GEN5_X16_GBPS, 4),
                              # NVML PCIe TX counter of this GPU over the timed steps, per step
-                             "traffic": None if pcie is None else round(pcie / args.steps),
-                             "traffic_source": "nvmlDeviceGetPcieThroughput(TX) sampled every 20 ms over the "
-                                               "timed steps (KB/s x dt), per step; algorithmic bytes per step "
-                                               "= payload",
+                             "traffic": None if pcie.bytes is None else round(pcie.bytes / args.steps),
+                             "traffic_source": "nvmlDeviceGetPcieThroughput(TX), 20 ms windows sampled back to "
+                                               "back over the timed steps and integrated, per step (includes "
+                                               "TLP/protocol overhead); algorithmic bytes per step = payload",
                              "peak_measured_dma": link["dma_gbps"],
                              "frac_of_measured_dma": round(per_gpu / link["dma_gbps"], 4),
                              "kernel": {"name": "lzk_gather_kernel", "achieved": kernel_gbps,
@@ -492,21 +489,44 @@ def main_ours(args, rank, world, local_rank):
         shutil.rmtree(tmp, ignore_errors=True)
 
 
-def pcie_tx_bytes(dev: int):
-    """Cumulative PCIe bytes this GPU has transmitted (NVML field
-    NVML_FI_DEV_PCIE_COUNT_TX_BYTES); None where NVML does not expose it."""
-    try:
-        import pynvml
-        import torch
-        pynvml.nvmlInit()
-        p = torch.cuda.get_device_properties(dev)
-        h = pynvml.nvmlDeviceGetHandleByPciBusId(f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0")
-        v = pynvml.nvmlDeviceGetFieldValues(h, [pynvml.NVML_FI_DEV_PCIE_COUNT_TX_BYTES])[0]
-        if v.nvmlReturn != 0:
-            return None
-        return int(v.value.ullVal)
-    except Exception:
-        return None
+class PcieSampler:
+    """PCIe bytes this GPU transmits (device -> host) while the block runs:
+    nvmlDeviceGetPcieThroughput(TX) (KB/s over NVML's 20 ms window) sampled
+    back to back on a thread and integrated over time. None where NVML does
+    not report it."""
+
+    def __init__(self, dev: int):
+        self.dev, self.bytes, self._stop, self._t = dev, None, threading.Event(), None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            p = torch.cuda.get_device_properties(self.dev)
+            self._h = pynvml.nvmlDeviceGetHandleByPciBusId(
+                f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0")
+            self._nvml = pynvml
+            pynvml.nvmlDeviceGetPcieThroughput(self._h, pynvml.NVML_PCIE_UTIL_TX_BYTES)
+        except Exception:
+            return self
+        self.bytes = 0.0
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def _run(self):
+        last = time.perf_counter()
+        while not self._stop.is_set():
+            kbps = self._nvml.nvmlDeviceGetPcieThroughput(self._h, self._nvml.NVML_PCIE_UTIL_TX_BYTES)
+            now = time.perf_counter()
+            self.bytes += kbps * 1e3 * (now - last)
+            last = now
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=5)
 
 
 def measure_streaming(lz, built, plan, payload, tmp, dev, barrier, producer, pool=16 << 30, segment=1 << 30):
@@ -623,14 +643,20 @@ def run_iterations(lz, torch, eng, plan, tree, gemm, opt, opt_region, n, every, 
     events on the compute stream; one host sync after the last iteration."""
     comp = gemm.stream
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1)]
-    fences, cap_ms, tickets = [], [], []
+    fences, gaps, cap_ms, tickets = [], [], [], []
     evs[0].record(comp)
     for i in range(n):
         t = None
         if every and i % every == 0:
+            # g0 -> g1 on the compute stream = how long the stream sat idle
+            # because the host was inside capture() (0 when it had queued work)
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(comp)
             h0 = time.perf_counter()
             t = eng.capture(plan, tree, step0 + i, producer_stream=comp)
             cap_ms.append((time.perf_counter() - h0) * 1e3)
+            g1.record(comp)
+            gaps.append((g0, g1))
         gemm.fwd_bwd()
         if t is not None:
             if fence == "device":
@@ -654,7 +680,8 @@ def run_iterations(lz, torch, eng, plan, tree, gemm, opt, opt_region, n, every, 
         assert not t.torn()
     it = [evs[i].elapsed_time(evs[i + 1]) for i in range(n)]
     fw = [a.elapsed_time(b) for a, b in fences]
-    return it, cap_ms, fw
+    gap = [a.elapsed_time(b) for a, b in gaps]
+    return it, cap_ms, fw, gap
 
 
 def train_stall(lz, torch, eng, plan, tree, gemm, barrier, step0):
@@ -668,16 +695,21 @@ def train_stall(lz, torch, eng, plan, tree, gemm, barrier, step0):
                                                      fence, s0)
     run(2, 0, "device", step0)
     base = run(5, 0, "device", step0 + 10)[0][1:]
-    it_dev, cap_dev, fw_dev = run(6, 1, "device", step0 + 20)
-    it_host, _, _ = run(4, 1, "host", step0 + 40)
+    it_dev, cap_dev, fw_dev, gap_dev = run(6, 1, "device", step0 + 20)
+    it_host = run(4, 1, "host", step0 + 40)[0]
     base_ms = statistics.mean(base)
     it_ms = statistics.mean(it_dev[1:])
     it_host_ms = statistics.mean(it_host[1:])
     return {"t_fwd_bwd_ms": round(gemm.t_fb_ms, 2), "iter_no_ckpt_ms": round(base_ms, 2),
             "iter_ckpt_ms": round(it_ms, 2), "stall_ms": round(it_ms - base_ms, 2),
             "capture_host_ms": round(statistics.mean(cap_dev[1:]), 3),
+            "capture_host_note": "host time inside capture(); in a loop with no host sync it includes waiting "
+                                 "for pool space (the previous snapshot) while the GPU still runs queued work",
+            "capture_gap_ms": round(statistics.mean(gap_dev[1:]), 3),
             "fence_wait_ms": round(statistics.mean(fw_dev[1:]), 3),
-            "stall_def_ms": round(statistics.mean(c + f for c, f in zip(cap_dev[1:], fw_dev[1:])), 3),
+            "stall_def_ms": round(statistics.mean(g + f for g, f in zip(gap_dev[1:], fw_dev[1:])), 3),
+            "stall_def": "compute-stream CUDA events: idle gap at capture() + wait at the lazy fence "
+                         "(SURVEY.md §8d: capture + fence, measured on the compute stream)",
             "iter_overhead": round((it_ms - base_ms) / base_ms, 4),
             "host_fence": {"iter_ckpt_ms": round(it_host_ms, 2), "stall_ms": round(it_host_ms - base_ms, 2),
                            "iter_overhead": round((it_host_ms - base_ms) / base_ms, 4)},
@@ -773,58 +805,88 @@ def durable_stall(lz, torch, sbuilt, tmp, dev, gemm, barrier, stall):
     pinned pool smaller than two checkpoints, so the flush backs up into
     capture() as in the reference's trainer loop (bench.cpp:261-313;
     buffer_pool.cpp:12-40). Shard = the matched sample (C2 itself does not
-    fit the box's local disk); fwd/bwd = the C2 GEMM loop. Measured stall per
-    iteration against the closed form max(0, S/b_flush - (t_f+t_b+t_u))
-    (simulator.cpp:62-63), and at the smallest interval K the
-    disk sustains, predicted max(0, S/b_flush - K*t_iter)/K."""
-    S = sbuilt.bytes
+    fit the box's local disk); fwd/bwd = the C2 GEMM loop. The measured stall
+    per iteration is set against the closed form max(0, S/b_flush - t_iter)
+    (simulator.cpp:62-63), b_flush being the rate the disk
+    sustains for back-to-back checkpoints measured just before, and at the
+    smallest interval K the disk sustains, max(0, S/b_flush - K*t_iter)/K."""
+    import queue
     root = os.path.join(tmp, "durable_ckpt")
-    cfg = lz.EngineConfig(checkpoint_root=root, host_buffer_bytes=int(S * 1.5) + (64 << 20),
-                          fsync_on_finalize=True, device=dev)
+    pool = int(sbuilt.bytes * 1.5) + (64 << 20)
+    cfg = lz.EngineConfig(checkpoint_root=root, host_buffer_bytes=pool, fsync_on_finalize=True, device=dev)
     eng = lz.Engine(cfg, sbuilt.topo, sbuilt.rank)
     plan = lz.plan_checkpoint(sbuilt.topo, sbuilt.model, sbuilt.step)
     r = sbuilt.rank
     rank_dir = f"rank-{r.dp}-{r.pp}-{r.tp}"
-    # b_flush: one checkpoint alone, capture -> durable
-    h0 = time.perf_counter()
-    t = eng.capture(plan, sbuilt.tree, 900, producer_stream=gemm.stream)
-    eng.update_barrier(t)
-    h1 = time.perf_counter()
-    eng.wait_persisted(t)
-    t_flush = time.perf_counter() - h1
-    shutil.rmtree(os.path.join(root, "step-900"), ignore_errors=True)
-    b_flush = S / t_flush
+    # persisted checkpoints leave the disk (it holds ~2 of them), off the loop's thread
+    doomed = queue.Queue()
+    reaper = threading.Thread(target=lambda: [shutil.rmtree(p, ignore_errors=True) for p in iter(doomed.get, None)],
+                              daemon=True)
+    reaper.start()
 
     def retire(tickets):
-        # persisted checkpoints leave the disk (it holds ~2 of them)
         while tickets and tickets[0].status() == "persisted":
-            shutil.rmtree(os.path.join(root, f"step-{tickets[0].step()}", rank_dir), ignore_errors=True)
+            doomed.put(os.path.join(root, f"step-{tickets[0].step()}", rank_dir))
             tickets.pop(0)
 
-    opt = torch.zeros(64 << 20, dtype=torch.float32, device="cuda")
-    opt_region = lz.DeviceRegion.wrap(opt)
-    run = lambda n, every, s0: run_iterations(lz, torch, eng, plan, sbuilt.tree, gemm, opt, opt_region, n, every,
-                                              "device", s0, retire)
-    barrier()
-    base = run(4, 0, 1000)[0][1:]
-    base_ms = statistics.mean(base)
-    t_iter = base_ms * 1e-3
-    every1 = run(7, 1, 1100)[0][2:]  # steady state after the pool has filled
-    pred1 = max(0.0, S / b_flush - t_iter)
-    K = max(1, math.ceil((S / b_flush) / t_iter))
-    everyK = run(max(4 * K, 6), K, 1200)[0][K:]
-    predK = max(0.0, S / b_flush - K * t_iter) / K
-    eng.close()
-    shutil.rmtree(root, ignore_errors=True)
+    try:
+        # b_flush: four checkpoints back to back with no compute; each capture
+        # waits in the pool for the previous flush, so this is the disk's
+        # sustained checkpoint rate (one file-set alone reads higher)
+        pending = []
+        h0 = time.perf_counter()
+        for k in range(4):
+            t = eng.capture(plan, sbuilt.tree, 900 + k, producer_stream=gemm.stream)
+            eng.update_barrier(t)
+            pending.append(t)
+            if k == 0:
+                eng.wait_persisted(t)
+                t_single = time.perf_counter() - h0
+                h1 = time.perf_counter()
+            retire(pending)
+        for t in pending:
+            eng.wait_persisted(t)
+        t_three = time.perf_counter() - h1
+        S = t.payload_bytes()
+        retire(pending)
+        b_flush = 3 * S / t_three
+        opt = torch.zeros(64 << 20, dtype=torch.float32, device="cuda")
+        opt_region = lz.DeviceRegion.wrap(opt)
+        run = lambda n, every, s0: run_iterations(lz, torch, eng, plan, sbuilt.tree, gemm, opt, opt_region, n,
+                                                  every, "device", s0, retire)
+        barrier()
+        base = run(4, 0, 1000)[0][1:]
+        base_ms = statistics.mean(base)
+        t_iter = base_ms * 1e-3
+        it1, cap1, _, gap1 = run(7, 1, 1100)
+        every1 = it1[2:]  # steady state after the pool has filled
+        pred1 = max(0.0, S / b_flush - t_iter)
+        K = max(1, math.ceil((S / b_flush) / t_iter))
+        itK = run(max(4 * K, 6), K, 1200)[0]
+        everyK = itK[K:]
+        predK = max(0.0, S / b_flush - K * t_iter) / K
+        log(f"[bench] durable: b_flush single {S / t_single / 1e9:.2f} sustained {b_flush / 1e9:.2f} GB/s; "
+            f"t_iter {base_ms:.0f} ms; every-1 iters {[round(x) for x in it1]} capture host "
+            f"{[round(x) for x in cap1]} gaps {[round(x) for x in gap1]}; every-{K} iters {[round(x) for x in itK]}")
+    finally:
+        eng.close()
+        doomed.put(None)
+        reaper.join(timeout=120)
+        shutil.rmtree(root, ignore_errors=True)
     m1 = statistics.mean(every1) - base_ms
     mK = statistics.mean(everyK) - base_ms
     return {"tier": "durable files: fsync, O_DIRECT interior, local disk",
-            "shard_bytes": S, "pool_bytes": int(S * 1.5) + (64 << 20),
-            "b_flush_gbps": round(b_flush / 1e9, 3), "t_iter_no_ckpt_ms": round(base_ms, 2),
+            "shard_bytes": S, "pool_bytes": pool,
+            "b_flush_gbps": round(b_flush / 1e9, 3),
+            "b_flush_single_gbps": round(S / t_single / 1e9, 3),
+            "b_flush_how": "sustained: 3 checkpoints back to back, each behind the previous flush (no compute); "
+                           "single = one checkpoint alone, capture -> persisted",
+            "t_iter_no_ckpt_ms": round(base_ms, 2),
             "every_1": {"stall_ms": round(m1, 1), "predicted_ms": round(pred1 * 1e3, 1),
-                        "iter_overhead": round(m1 / base_ms, 4)},
+                        "iter_overhead": round(m1 / base_ms, 4),
+                        "iters_ms": [round(x, 1) for x in it1]},
             f"every_{K}": {"K": K, "stall_ms_per_iter": round(mK, 1), "predicted_ms_per_iter": round(predK * 1e3, 1),
-                           "iter_overhead": round(mK / base_ms, 4)},
+                           "iter_overhead": round(mK / base_ms, 4), "iters_ms": [round(x, 1) for x in itK]},
             "closed_form": "every 1: S/b_flush - (t_f+t_b+t_u); every K: max(0, S/b_flush - K*t_iter)/K",
             "note": "C2 (108 GB) exceeds the box's 80 GB disk; the shard is the matched sample, the GEMM loop C2's"}
 
