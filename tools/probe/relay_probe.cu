@@ -1,0 +1,93 @@
+// Uplink-relay probe (one process, two GPUs): can GPU B carry GPU A's
+// snapshot bytes to host memory over B's own PCIe link, reading A's HBM over
+// NVLink? Measures, with CUDA events, 8 GiB device->pinned host:
+//   a   A's copy engine, A's memory -> host
+//   b   B's copy engine, A's memory (peer) -> host
+//   ab  a and b at once on disjoint halves (aggregate)
+//   k   a gather-style SM kernel on B reading A's memory, storing to host
+//   ak  a (copy engine on A) and k at once
+// Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o relay_probe relay_probe.cu
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#define CK(x)                                                                                     \
+  do {                                                                                            \
+    cudaError_t e_ = (x);                                                                         \
+    if (e_ != cudaSuccess) {                                                                      \
+      std::fprintf(stderr, "%s:%d %s: %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e_));     \
+      std::exit(1);                                                                               \
+    }                                                                                             \
+  } while (0)
+
+__global__ void copy_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, size_t n16) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n16; i += size_t(gridDim.x) * blockDim.x) {
+    dst[i] = src[i];
+  }
+}
+
+double now() { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); }
+
+int main(int argc, char** argv) {
+  const int A = argc > 1 ? std::atoi(argv[1]) : 0;
+  const int B = argc > 2 ? std::atoi(argv[2]) : 1;
+  const size_t bytes = 8ull << 30, chunk = 256ull << 20;
+  int can = 0;
+  CK(cudaDeviceCanAccessPeer(&can, B, A));
+  std::printf("peer access %d -> %d: %d\n", B, A, can);
+  void* src = nullptr;
+  CK(cudaSetDevice(A));
+  CK(cudaMalloc(&src, bytes));
+  CK(cudaMemset(src, 0x5a, bytes));
+  void* host = nullptr;
+  CK(cudaHostAlloc(&host, bytes, cudaHostAllocPortable | cudaHostAllocMapped));
+  CK(cudaSetDevice(B));
+  if (can) CK(cudaDeviceEnablePeerAccess(A, 0));
+  cudaStream_t sa, sb;
+  CK(cudaSetDevice(A));
+  CK(cudaStreamCreateWithFlags(&sa, cudaStreamNonBlocking));
+  CK(cudaSetDevice(B));
+  CK(cudaStreamCreateWithFlags(&sb, cudaStreamNonBlocking));
+
+  auto ce = [&](cudaStream_t s, int dev, size_t off, size_t len) {
+    CK(cudaSetDevice(dev));
+    for (size_t o = 0; o < len; o += chunk) {
+      CK(cudaMemcpyAsync(static_cast<char*>(host) + off + o, static_cast<char*>(src) + off + o,
+                         std::min(chunk, len - o), cudaMemcpyDefault, s));
+    }
+  };
+  auto kern = [&](size_t off, size_t len) {
+    CK(cudaSetDevice(B));
+    copy_kernel<<<16, 512, 0, sb>>>(reinterpret_cast<const uint4*>(static_cast<char*>(src) + off),
+                                    reinterpret_cast<uint4*>(static_cast<char*>(host) + off), len / 16);
+    CK(cudaGetLastError());
+  };
+  auto sync = [&] {
+    CK(cudaStreamSynchronize(sa));
+    CK(cudaStreamSynchronize(sb));
+  };
+  auto run = [&](const char* name, auto fn, size_t moved) {
+    fn();
+    sync();  // warm-up
+    double best = 0;
+    for (int r = 0; r < 4; ++r) {
+      const double t0 = now();
+      fn();
+      sync();
+      best = std::max(best, moved / (now() - t0) / 1e9);
+    }
+    std::printf("%-4s %8.2f GB/s\n", name, best);
+  };
+  run("a", [&] { ce(sa, A, 0, bytes); }, bytes);
+  run("b", [&] { ce(sb, B, 0, bytes); }, bytes);
+  run("ab", [&] { ce(sa, A, 0, bytes / 2); ce(sb, B, bytes / 2, bytes / 2); }, bytes);
+  run("ab31", [&] { ce(sa, A, 0, bytes / 4 * 3); ce(sb, B, bytes / 4 * 3, bytes / 4); }, bytes);
+  if (can) {
+    run("k", [&] { kern(0, bytes); }, bytes);
+    run("ak", [&] { ce(sa, A, 0, bytes / 2); kern(bytes / 2, bytes / 2); }, bytes);
+  }
+  return 0;
+}
