@@ -107,6 +107,10 @@ constexpr uint32_t kTile = 16u << 10;      // bytes of one descriptor per WARP w
 constexpr int kThreads = 512;              // 16 warps per CTA
 constexpr int kWarps = kThreads / 32;
 constexpr int kUnroll = 4;                 // 16-byte words in flight per lane per pass
+// Skewed copies hold two source words per output word: half the unroll keeps
+// the kernel inside 128 registers (no spills) with ~256 KB still in flight
+// across 8 CTAs, above the host link's bandwidth-delay product (~100 KB).
+constexpr int kUnrollSkew = 2;
 constexpr uint32_t kMaxDescPerLaunch = 960;
 
 struct Desc {
@@ -163,10 +167,10 @@ __device__ __forceinline__ uint4 extract(const uint4& a, const uint4& b, uint32_
 template <int Q>
 __device__ __forceinline__ void body_skewed(const uint4* __restrict__ sa, uint4* dw, uint32_t nw,
                                             uint32_t shift, uint32_t lane) {
-  for (uint32_t base = lane; base < nw; base += 32 * kUnroll) {
-    uint4 lo[kUnroll], hi[kUnroll];
+  for (uint32_t base = lane; base < nw; base += 32 * kUnrollSkew) {
+    uint4 lo[kUnrollSkew], hi[kUnrollSkew];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < kUnrollSkew; ++u) {
       const uint32_t j = base + u * 32;
       if (j < nw) {
         lo[u] = ld_cached(sa + j);
@@ -174,7 +178,7 @@ __device__ __forceinline__ void body_skewed(const uint4* __restrict__ sa, uint4*
       }
     }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < kUnrollSkew; ++u) {
       const uint32_t j = base + u * 32;
       if (j < nw) st_word(dw + j, extract<Q>(lo[u], hi[u], shift));
     }
