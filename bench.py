@@ -463,10 +463,10 @@ def main_ours(args, rank, world, local_rank):
                                         "peak_measured_sm_store": link["sm_store_gbps"],
                                         "frac_of_measured_sm_store": round(kernel_gbps / link["sm_store_gbps"], 4),
                                         # one `ncu --set full` capture of a 62.92 MB launch
-                                        # (profiles/r01_gather_kernel_ncu.md, v3): DRAM read +
-                                        # write per launch vs the algorithmic bytes
-                                        "traffic": 62.9248e6 + 0.3566e6, "algorithmic_bytes_per_launch": 62.92e6,
-                                        "ncu_profile": "profiles/r01_gather_kernel_ncu.md"},
+                                        # (profiles/r02_gather_kernel_ncu.md, aligned class):
+                                        # DRAM read + write per launch vs the algorithmic bytes
+                                        "traffic": 62.923e6 + 1.204e6, "algorithmic_bytes_per_launch": 62.92e6,
+                                        "ncu_profile": "profiles/r02_gather_kernel_ncu.md"},
                              "link_probe": link["how"],
                              "link_probes_per_rank": [{k: l[k] for k in ("dma_gbps", "sm_store_gbps", "numa_node")}
                                                       for l in links],
