@@ -4,8 +4,8 @@ Times the bench's synthetic fwd/bwd (bf16 8192^3 GEMMs on a compute stream)
   B: with a raw copy-engine D2H of the same bytes on a side stream (torch
      non_blocking copies into pinned memory; no engine, no host threads),
   C: with an Engine capture of the C2 shard (the bench's configuration),
-  D: the same with every byte forced through lzk_gather_kernel (8 CTAs):
-     the SM time the kernel variant takes from the trainer.
+  D: the same with every byte forced through lzk_gather_kernel (2, 4 and 8
+     CTAs): the SM time the kernel variant takes from the trainer, by grid.
 Prints one JSON line; B - A is hardware interference, C - B the engine's own.
     python tools/interference.py [layers]"""
 import json
@@ -66,8 +66,10 @@ def run(mode):
     torch.cuda.synchronize()
     h0 = time.perf_counter()
     t = None
-    if mode in ("engine", "engine_kernel"):
-        eng.set_copy_variant(force_kernel=mode == "engine_kernel", force_copy_engine=False)
+    if mode.startswith("engine"):
+        kernel = mode.startswith("engine_kernel")
+        ctas = int(mode.rsplit("_", 1)[1]) if kernel else 8
+        eng.set_copy_variant(force_kernel=kernel, force_copy_engine=False, kernel_ctas=ctas)
         t = eng.capture(plan, built.tree, int(time.time() * 1000) % 1000000 + 1)
     elif mode == "raw_dma":
         with torch.cuda.stream(side):
@@ -88,7 +90,7 @@ def run(mode):
 
 
 res = {}
-for mode in ("alone", "raw_dma", "engine", "engine_kernel") * 3:
+for mode in ("alone", "raw_dma", "engine", "engine_kernel_2", "engine_kernel_4", "engine_kernel_8") * 3:
     g, wall = run(mode)
     res.setdefault(mode, []).append((g, wall))
 out = {"n_mm": n_mm, "per_mm_ms": round(per_mm, 4), "payload": payload}
@@ -97,6 +99,7 @@ for k, v in res.items():
               "wall_ms": round(statistics.median(x[1] for x in v), 2)}
 out["hw_interference_ms"] = round(out["raw_dma"]["gemm_ms"] - out["alone"]["gemm_ms"], 2)
 out["engine_extra_ms"] = round(out["engine"]["gemm_ms"] - out["raw_dma"]["gemm_ms"], 2)
-out["kernel_variant_extra_ms"] = round(out["engine_kernel"]["gemm_ms"] - out["alone"]["gemm_ms"], 2)
+for c in (2, 4, 8):
+    out[f"kernel_variant_extra_ms_{c}ctas"] = round(out[f"engine_kernel_{c}"]["gemm_ms"] - out["alone"]["gemm_ms"], 2)
 print(json.dumps(out))
 eng.close()
