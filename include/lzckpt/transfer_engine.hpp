@@ -103,7 +103,9 @@ struct ThrottledChannel {
 struct SnapshotOptions {
   int device = -1;                    // -1: current device at construction
   uint64_t ce_threshold = 2ull << 20; // tasks >= this go to the copy engines
-  uint32_t kernel_ctas = 8;           // gather kernel grid: 4 saturate PCIe for every size class
+  // gather kernel grid: 2 CTAs already saturate the host link in every size
+  // class (profiles/r02_ctasweep.jsonl); 4 leave margin and take 2.7 % of the SMs
+  uint32_t kernel_ctas = 4;
   uint64_t group_bytes = 256ull << 20; // bytes per completion event (and max DMA size)
   // > 0: the least priority, < 0: the greatest. CUDA's least priority IS the
   // default (0), so the snapshot stream never ranks below an ordinary compute

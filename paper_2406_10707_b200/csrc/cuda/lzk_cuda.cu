@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(kThreads)
 int launch_gather(cudaStream_t stream, const lzk_copy_desc* d, uint32_t n, uint32_t max_ctas) {
   if (n == 0) return LZK_OK;
   if (d == nullptr) return fail(LZK_ERR_INVALID, "gather: null descriptor array");
-  if (max_ctas == 0) max_ctas = 8;
+  if (max_ctas == 0) max_ctas = 4;  // 2 saturate the host link (profiles/r02_ctasweep.jsonl)
   // Stack-allocating 31 KB is fine for host threads; keep it static per thread.
   thread_local DescBatch batch;
   uint32_t i = 0;

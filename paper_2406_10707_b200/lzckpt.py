@@ -548,7 +548,7 @@ class EngineConfig:
     reserve_timeout_ms: int = 60_000
     device: int = -1
     ce_threshold: int = 2 << 20
-    kernel_ctas: int = 8
+    kernel_ctas: int = 4
     group_bytes: int = 256 << 20
     force_kernel: bool = False
     force_copy_engine: bool = False
