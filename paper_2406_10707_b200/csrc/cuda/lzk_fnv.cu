@@ -53,8 +53,14 @@ using lzk_detail::fail;
 using lzk_detail::use_device;
 
 constexpr uint64_t kPrime = 0x100000001b3ull;
-constexpr int kHashThreads = 512;
+// Small CTAs (4 warps, up to 8 resident per SM at 64 registers) let the block
+// scheduler spread one-warp-per-range work evenly over the SMs: with 512-thread
+// CTAs, 4096 ranges filled 108 SMs with 32 warps and 40 with 16.
+constexpr int kHashThreads = 128;
 constexpr int kHashWarps = kHashThreads / 32;
+constexpr uint32_t kCtasPerSm = 8;
+// the C ABI's max_ctas counts 512-thread CTA equivalents (about one SM each)
+constexpr uint32_t kCtaScale = 512 / kHashThreads;
 constexpr uint64_t kSegMin = 256ull << 10;  // bytes, multiple of 1 KiB
 constexpr uint32_t kMaxSegs = 2048;         // per range
 constexpr uint64_t kLongMin = 4ull << 20;
@@ -394,7 +400,7 @@ __global__ void __launch_bounds__(kHashThreads) lzk_fnv_pass_kernel(const HashBa
 
 // Final pass: short ranges are hashed whole (result stored to out); every
 // segment of a long range is hashed from its incoming low byte.
-__global__ void __launch_bounds__(kHashThreads, 2) lzk_fnv_kernel(const HashBatch batch, Scratch sc) {
+__global__ void __launch_bounds__(kHashThreads, kCtasPerSm) lzk_fnv_kernel(const HashBatch batch, Scratch sc) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt = (1u << lane) - 1u;
   const uint32_t nwarps = gridDim.x * kHashWarps;
@@ -504,7 +510,7 @@ int launch_hash(cudaStream_t stream, int device, const lzk_hash_desc* d, uint32_
     total += d[i].len;
   }
   set_pool_threshold(device);
-  const uint32_t ctas = max_ctas ? max_ctas : uint32_t(sm_count(device)) * 2;
+  const uint32_t ctas = max_ctas ? max_ctas * kCtaScale : uint32_t(sm_count(device)) * kCtasPerSm;
   const uint64_t fair = total / (uint64_t(ctas) * kHashWarps);
   // largest first, dealt round-robin to warps (longest-processing-time order)
   std::vector<uint32_t> order(n);
