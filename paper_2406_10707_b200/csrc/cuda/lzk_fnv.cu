@@ -53,14 +53,18 @@ using lzk_detail::fail;
 using lzk_detail::use_device;
 
 constexpr uint64_t kPrime = 0x100000001b3ull;
-// Small CTAs (4 warps, up to 8 resident per SM at 64 registers) let the block
-// scheduler spread one-warp-per-range work evenly over the SMs: with 512-thread
-// CTAs, 4096 ranges filled 108 SMs with 32 warps and 40 with 16.
-constexpr int kHashThreads = 128;
-constexpr int kHashWarps = kHashThreads / 32;
-constexpr uint32_t kCtasPerSm = 8;
-// the C ABI's max_ctas counts 512-thread CTA equivalents (about one SM each)
-constexpr uint32_t kCtaScale = 512 / kHashThreads;
+// Two CTA shapes, same 32 resident warps per SM at 64 registers:
+//  * short ranges only (one warp per range): 128-thread CTAs, 8 per SM, so the
+//    block scheduler spreads the warps evenly (512-thread CTAs put 4096 ranges
+//    on 108 SMs with 32 warps and 40 with 16: uniform 1 MiB ranges 1.26 ->
+//    1.33 TB/s);
+//  * batches with segmented long ranges: 512-thread CTAs, 2 per SM (their
+//    multi-pass schedule measured ~9 % faster that way).
+// The C ABI's max_ctas counts 512-thread CTA equivalents (about one SM each).
+constexpr int kBigThreads = 512;
+constexpr int kSmallThreads = 128;
+constexpr uint32_t kWarpsPerSm = 32;
+constexpr int kHashWarps = kBigThreads / 32;  // warps per max_ctas unit
 constexpr uint64_t kSegMin = 256ull << 10;  // bytes, multiple of 1 KiB
 constexpr uint32_t kMaxSegs = 2048;         // per range
 constexpr uint64_t kLongMin = 4ull << 20;
@@ -366,11 +370,12 @@ __device__ __forceinline__ uint32_t parity_prefix(const uint8_t* par, uint32_t b
 // Pass I of the long-range schedule: plane-I parity of every segment that
 // has a successor.
 template <int I>
-__global__ void __launch_bounds__(kHashThreads) lzk_fnv_pass_kernel(const HashBatch batch, Scratch sc) {
+__global__ void __launch_bounds__(kBigThreads) lzk_fnv_pass_kernel(const HashBatch batch, Scratch sc) {
+  constexpr uint32_t kWarps = kBigThreads / 32;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt = (1u << lane) - 1u;
-  const uint32_t nwarps = gridDim.x * kHashWarps;
-  for (uint32_t t = blockIdx.x * kHashWarps + (threadIdx.x >> 5); t < batch.total_segs; t += nwarps) {
+  const uint32_t nwarps = gridDim.x * kWarps;
+  for (uint32_t t = blockIdx.x * kWarps + (threadIdx.x >> 5); t < batch.total_segs; t += nwarps) {
     const HashItem it = batch.it[find_item(batch, t)];
     const uint32_t s = t - it.seg_begin;
     if (s + 1 >= it.nseg) continue;  // nobody consumes the last segment's parity
@@ -400,12 +405,14 @@ __global__ void __launch_bounds__(kHashThreads) lzk_fnv_pass_kernel(const HashBa
 
 // Final pass: short ranges are hashed whole (result stored to out); every
 // segment of a long range is hashed from its incoming low byte.
-__global__ void __launch_bounds__(kHashThreads, kCtasPerSm) lzk_fnv_kernel(const HashBatch batch, Scratch sc) {
+template <int T>
+__global__ void __launch_bounds__(T, kWarpsPerSm * 32 / T) lzk_fnv_kernel(const HashBatch batch, Scratch sc) {
+  constexpr uint32_t kWarps = T / 32;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt = (1u << lane) - 1u;
-  const uint32_t nwarps = gridDim.x * kHashWarps;
+  const uint32_t nwarps = gridDim.x * kWarps;
   const uint64_t wlane = pow64(kPrime, 32u * (31u - lane));
-  for (uint32_t t = blockIdx.x * kHashWarps + (threadIdx.x >> 5); t < batch.total_segs; t += nwarps) {
+  for (uint32_t t = blockIdx.x * kWarps + (threadIdx.x >> 5); t < batch.total_segs; t += nwarps) {
     const HashItem it = batch.it[find_item(batch, t)];
     const uint32_t s = t - it.seg_begin;
     const uint8_t* src = reinterpret_cast<const uint8_t*>(it.d.src);
@@ -480,7 +487,7 @@ int sm_count(int device) {
 
 template <int I>
 void launch_pass(uint32_t grid, cudaStream_t s, const HashBatch& b, Scratch sc) {
-  lzk_fnv_pass_kernel<I><<<grid, kHashThreads, 0, s>>>(b, sc);
+  lzk_fnv_pass_kernel<I><<<grid, kBigThreads, 0, s>>>(b, sc);
 }
 
 void set_pool_threshold(int device) {
@@ -510,7 +517,7 @@ int launch_hash(cudaStream_t stream, int device, const lzk_hash_desc* d, uint32_
     total += d[i].len;
   }
   set_pool_threshold(device);
-  const uint32_t ctas = max_ctas ? max_ctas * kCtaScale : uint32_t(sm_count(device)) * kCtasPerSm;
+  const uint32_t ctas = max_ctas ? max_ctas : uint32_t(sm_count(device)) * (kWarpsPerSm / kHashWarps);
   const uint64_t fair = total / (uint64_t(ctas) * kHashWarps);
   // largest first, dealt round-robin to warps (longest-processing-time order)
   std::vector<uint32_t> order(n);
@@ -566,6 +573,10 @@ int launch_hash(cudaStream_t stream, int device, const lzk_hash_desc* d, uint32_
     }
   }
   const uint32_t grid = std::max(1u, std::min<uint32_t>((segs + kHashWarps - 1) / kHashWarps, ctas));
+  constexpr uint32_t kSmallPerBig = kBigThreads / kSmallThreads;
+  const uint32_t small_warps = kSmallThreads / 32;
+  const uint32_t small_grid =
+      std::max(1u, std::min<uint32_t>((segs + small_warps - 1) / small_warps, ctas * kSmallPerBig));
   if (any_long) {
     launch_pass<0>(grid, stream, batch, sc);
     launch_pass<1>(grid, stream, batch, sc);
@@ -577,7 +588,11 @@ int launch_hash(cudaStream_t stream, int device, const lzk_hash_desc* d, uint32_
     launch_pass<7>(grid, stream, batch, sc);
     launches += 8;
   }
-  lzk_fnv_kernel<<<grid, kHashThreads, 0, stream>>>(batch, sc);
+  if (any_long) {
+    lzk_fnv_kernel<kBigThreads><<<grid, kBigThreads, 0, stream>>>(batch, sc);
+  } else {
+    lzk_fnv_kernel<kSmallThreads><<<small_grid, kSmallThreads, 0, stream>>>(batch, sc);
+  }
   ++launches;
   if (any_long) {
     lzk_fnv_combine_kernel<<<(n + 7) / 8, 256, 0, stream>>>(batch, sc);
