@@ -195,8 +195,11 @@ class TransferEngine {
   // leaves (the reference clones them at capture, engine.cpp:138-143; here
   // that read is deferred behind the producer instead of blocking the
   // trainer). Call before the ticket's first submit_copies.
+  // `keep` holds the inline descriptors' destinations (the __meta__ buffers)
+  // until the gather has completed, even if the capture is abandoned.
   void set_prologue(uint64_t ticket, void* producer_stream, std::vector<lzk_copy_desc> inline_descs,
-                    std::vector<std::shared_ptr<DeviceRegion>> inline_regions);
+                    std::vector<std::shared_ptr<DeviceRegion>> inline_regions,
+                    std::vector<std::shared_ptr<const void>> keep = {});
   bool ticket_complete(uint64_t ticket) const;
   // Device time of a completed ticket's snapshot (CUDA events on the snapshot
   // stream, first device op -> last completion); < 0 when not measured.
@@ -257,6 +260,7 @@ class TransferEngine {
     std::vector<lzk_copy_desc> inline_descs;
     bool prologue = false;                 // the ticket's __meta__ is written on the device
     std::vector<InlineWatch> inline_watch;  // verdict at the first completed group
+    std::vector<std::shared_ptr<const void>> inline_keep;  // until the first group completes
   };
 
   void issuer_loop();

@@ -395,7 +395,9 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
     tickets_.emplace(ticket->id_, ticket);
   }
   if (deferred_inline) {
-    transfers_.set_prologue(ticket->id_, producer.stream, std::move(inl), std::move(inl_regions));
+    std::vector<std::shared_ptr<const void>> keep;
+    for (const auto& b : builds) keep.push_back(b.meta);  // the gather writes into every file's __meta__
+    transfers_.set_prologue(ticket->id_, producer.stream, std::move(inl), std::move(inl_regions), std::move(keep));
   } else if (producer.ordered) {
     // paced channel: its host-driven reads are ordered by a host wait here
     ck(lzk_stream_wait_raw(inline_stream_, producer.stream), "capture: producer wait");

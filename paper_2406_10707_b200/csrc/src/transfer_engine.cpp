@@ -239,7 +239,8 @@ void TransferEngine::submit_copies(uint64_t ticket, std::vector<std::shared_ptr<
 }
 
 void TransferEngine::set_prologue(uint64_t ticket, void* producer_stream, std::vector<lzk_copy_desc> inline_descs,
-                                  std::vector<std::shared_ptr<DeviceRegion>> inline_regions) {
+                                  std::vector<std::shared_ptr<DeviceRegion>> inline_regions,
+                                  std::vector<std::shared_ptr<const void>> keep) {
   if (channel_.bandwidth_Bps > 0) throw Error("set_prologue: the paced channel is host-driven");
   lzk_event* e = take_event();
   if (int rc = lzk_event_record_raw(e, producer_stream); rc != LZK_OK) {
@@ -253,6 +254,7 @@ void TransferEngine::set_prologue(uint64_t ticket, void* producer_stream, std::v
   tp.producer = e;
   tp.inline_descs = std::move(inline_descs);
   tp.prologue = true;
+  tp.inline_keep = std::move(keep);
   tp.inline_watch.clear();
   tp.inline_watch.reserve(inline_regions.size());
   for (auto& r : inline_regions) {
@@ -472,6 +474,7 @@ void TransferEngine::run_device_group(Group& g) {
     // The prologue's inline gather ran before this group on the stream: its
     // verdict is due at the ticket's first completed group.
     auto& tp = tickets_[g.ticket];
+    tp.inline_keep.clear();  // the prologue's gather ran before this group
     if (!tp.inline_watch.empty()) {
       for (const auto& w : tp.inline_watch) {
         const uint64_t seen = w.fenced ? w.fence : w.region->version();
