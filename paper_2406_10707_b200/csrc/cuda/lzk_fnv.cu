@@ -31,13 +31,18 @@
 //  * short ranges: one warp per range (largest first, round-robin), one pass;
 //    about 16 integer ops per byte;
 //  * long ranges (more than a fair share of the grid, >= 4 MiB): split into
-//    up to 2048 segments of >= 256 KiB, all processed in parallel. Pass i
-//    (i = 0..7) gives every segment's plane-i parity, with the carry-in bits
-//    < i taken from the XOR of the earlier segments' parities (bit i of a
-//    segment's outgoing low byte depends only on incoming bits <= i). A final
-//    pass hashes every segment from its now-known incoming low byte, and one
-//    warp per range folds the segments affinely (h = P^len h + S). It costs
-//    about 4x the work of one pass, but one range can fill the GPU.
+//    up to 2048 segments of >= 256 KiB, all processed in parallel. Bit i of
+//    a segment's outgoing low byte depends only on incoming bits <= i, so
+//    plane parities can be resolved from the bottom up. Dual pass K
+//    (K = 0..3) takes the carry-in bits < 2K from the XOR of the earlier
+//    segments' parities and yields every segment's plane-2K parity and its
+//    plane-(2K+1) parity under both values of incoming bit 2K (a flipped
+//    bit 2K complements the whole x_{2K} plane); a one-warp-per-range
+//    resolve kernel then picks the right hypothesis in segment order. A
+//    final pass hashes every segment from its now-known incoming low byte,
+//    and one warp per range folds the segments affinely (h = P^len h + S).
+//    Four dual passes do 24 plane scans per window where eight single-plane
+//    passes did 36 (tools/fnv_scan_model.py models both schedules).
 #include <algorithm>
 #include <cstdint>
 #include <mutex>
@@ -324,6 +329,7 @@ __device__ uint64_t hash_range(const uint8_t* p, uint64_t n, uint64_t h, uint32_
 struct Scratch {
   uint8_t* par;  // per segment: bit i = plane-i parity of the segment
   uint64_t* S;   // per segment: true state after segment 0 / relative sum of the others
+  uint8_t* alt;  // per segment: bit 2K+1 = plane-(2K+1) parity if incoming bit 2K were 1
 };
 
 __device__ __forceinline__ uint32_t find_item(const HashBatch& b, uint32_t t) {
@@ -367,10 +373,81 @@ __device__ __forceinline__ uint32_t parity_prefix(const uint8_t* par, uint32_t b
   return x;
 }
 
-// Pass I of the long-range schedule: plane-I parity of every segment that
-// has a successor.
-template <int I>
-__global__ void __launch_bounds__(kBigThreads) lzk_fnv_pass_kernel(const HashBatch batch, Scratch sc) {
+__device__ __forceinline__ uint32_t prefix_xor(uint32_t p) {
+  p ^= p << 1;
+  p ^= p << 2;
+  p ^= p << 4;
+  p ^= p << 8;
+  p ^= p << 16;
+  return p;
+}
+
+// One full window of a dual pass: planes 0..2K resolved as in scan_planes
+// (carry-ins from `carry`), then plane 2K+1's parity for BOTH values of the
+// plane-2K carry-in, which this pass does not know yet. A different incoming
+// bit 2K flips the whole x_{2K} plane (x = l ^ b, and l_{2K} = carry ^ prefix),
+// so the second hypothesis is the column adder evaluated on ~x_{2K}. A plane's
+// parity does not depend on its own carry-in, so carry[2K+1] (hypothesis 0)
+// and `alt` (hypothesis 1) both start at 0.
+template <int K>
+__device__ __forceinline__ void scan_dual(const uint32_t* w, uint32_t* carry, uint32_t& alt, uint32_t lt) {
+  uint32_t B[8];
+  to_planes(w, B);
+  auto plane = [&](int i, uint32_t e) -> uint32_t {
+    const uint32_t p = prefix_xor(e);
+    const uint32_t bal = __ballot_sync(0xffffffffu, p >> 31);
+    const uint32_t cin = (__popc(bal & lt) ^ carry[i]) & 1u;
+    carry[i] ^= __popc(bal) & 1u;
+    return (p << 1) ^ (cin * 0xffffffffu) ^ B[i];
+  };
+  auto parity = [&](uint32_t e, uint32_t& c) {
+    c ^= __popc(__ballot_sync(0xffffffffu, prefix_xor(e) >> 31)) & 1u;
+  };
+  const uint32_t x0 = plane(0, B[0]);
+  if constexpr (K == 0) {
+    parity(B[1] ^ x0, carry[1]);
+    parity(B[1] ^ ~x0, alt);
+    return;
+  }
+  const uint32_t x1 = plane(1, B[1] ^ x0);
+  const uint32_t c2 = x1 & x0;
+  const uint32_t x2 = plane(2, B[2] ^ x1 ^ c2);
+  if constexpr (K == 1) {
+    auto e3 = [&](uint32_t x) { return B[3] ^ x ^ maj3(x, x1, c2); };
+    parity(e3(x2), carry[3]);
+    parity(e3(~x2), alt);
+    return;
+  }
+  const uint32_t c3 = maj3(x2, x1, c2);
+  const uint32_t x3 = plane(3, B[3] ^ x2 ^ c3);
+  const uint32_t c4 = maj3(x3, x2, c3);
+  const uint32_t x4 = plane(4, B[4] ^ x3 ^ x0 ^ c4);
+  auto e5 = [&](uint32_t x) { return B[5] ^ x ^ x1 ^ x0 ^ maj3(x, x3, x0) ^ ((x ^ x3 ^ x0) & c4); };
+  if constexpr (K == 2) {
+    parity(e5(x4), carry[5]);
+    parity(e5(~x4), alt);
+    return;
+  }
+  const uint32_t k1 = maj3(x4, x3, x0), k2 = (x4 ^ x3 ^ x0) & c4;
+  const uint32_t x5 = plane(5, e5(x4));
+  const uint32_t s1 = x5 ^ x4 ^ x1, m1 = maj3(x5, x4, x1);
+  const uint32_t s2 = x0 ^ k1 ^ k2, m2 = maj3(x0, k1, k2);
+  const uint32_t m3 = s1 & s2;
+  const uint32_t x6 = plane(6, B[6] ^ x5 ^ x2 ^ x1 ^ m1 ^ m2 ^ m3);
+  const uint32_t t2 = x1 ^ m1 ^ m2, n2 = maj3(x1, m1, m2);
+  auto e7 = [&](uint32_t x) {
+    const uint32_t t1 = x ^ x5 ^ x2;
+    return B[7] ^ x ^ x3 ^ x2 ^ x0 ^ maj3(x, x5, x2) ^ n2 ^ maj3(m3, t1, t2);
+  };
+  parity(e7(x6), carry[7]);
+  parity(e7(~x6), alt);
+}
+
+// Dual pass K of the long-range schedule (four instead of eight passes): for
+// every segment with a successor, the plane-2K parity and the plane-(2K+1)
+// parity under both values of the still-unknown incoming bit 2K.
+template <int K>
+__global__ void __launch_bounds__(kBigThreads) lzk_fnv_dual_pass_kernel(const HashBatch batch, Scratch sc) {
   constexpr uint32_t kWarps = kBigThreads / 32;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt = (1u << lane) - 1u;
@@ -378,14 +455,16 @@ __global__ void __launch_bounds__(kBigThreads) lzk_fnv_pass_kernel(const HashBat
   for (uint32_t t = blockIdx.x * kWarps + (threadIdx.x >> 5); t < batch.total_segs; t += nwarps) {
     const HashItem it = batch.it[find_item(batch, t)];
     const uint32_t s = t - it.seg_begin;
-    if (s + 1 >= it.nseg) continue;  // nobody consumes the last segment's parity
+    if (s + 1 >= it.nseg) continue;  // nobody consumes the last segment's parities
     const uint8_t* src = reinterpret_cast<const uint8_t*>(it.d.src);
     const uint32_t head = head_len(it.d.src, it.d.len);
     const uint64_t hh = fold_bytes(it.d.seed, src, head);
-    const uint32_t cin = (static_cast<uint32_t>(hh) ^ parity_prefix(sc.par, it.seg_begin, s, lane)) & ((1u << I) - 1u);
+    const uint32_t cin =
+        (static_cast<uint32_t>(hh) ^ parity_prefix(sc.par, it.seg_begin, s, lane)) & ((1u << (2 * K)) - 1u);
     uint32_t carry[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) carry[i] = (cin >> i) & 1u;  // bit I starts at 0
+    for (int i = 0; i < 8; ++i) carry[i] = (cin >> i) & 1u;  // bits 2K and 2K+1 start at 0
+    uint32_t alt = 0;
     const uint4* q = reinterpret_cast<const uint4*>(src + head + uint64_t(s) * it.seglen) + 2 * lane;
     const uint64_t windows = it.seglen >> 10;
     uint4 a = ld_nc(q), b = ld_nc(q + 1);
@@ -396,10 +475,41 @@ __global__ void __launch_bounds__(kBigThreads) lzk_fnv_pass_kernel(const HashBat
         a = ld_nc(q);
         b = ld_nc(q + 1);
       }
-      uint32_t l0, l16;
-      scan_planes<I + 1>(w, carry, lt, 0xffffffffu, l0, l16);
+      scan_dual<K>(w, carry, alt, lt);
     }
-    if (lane == 0) sc.par[t] |= static_cast<uint8_t>(carry[I] << I);
+    if (lane == 0) {
+      sc.par[t] |= static_cast<uint8_t>((carry[2 * K] << (2 * K)) | (carry[2 * K + 1] << (2 * K + 1)));
+      sc.alt[t] |= static_cast<uint8_t>(alt << (2 * K + 1));
+    }
+  }
+}
+
+// After dual pass K: walk each long range's segments in order (32 at a time,
+// ballot prefix), learn every segment's incoming bit 2K from the plane-2K
+// parities, and keep the matching plane-(2K+1) hypothesis in `par`. One warp
+// per range.
+template <int K>
+__global__ void lzk_fnv_resolve_kernel(const HashBatch batch, Scratch sc) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < batch.n; i += nwarps) {
+    const HashItem it = batch.it[i];
+    if (it.nseg == 1) continue;
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(it.d.src);
+    uint32_t bit = (static_cast<uint32_t>(fold_bytes(it.d.seed, src, head_len(it.d.src, it.d.len))) >> (2 * K)) & 1u;
+    for (uint32_t base = 0; base + 1 < it.nseg; base += 32) {
+      const uint32_t s = base + lane;
+      const bool mine = s + 1 < it.nseg;
+      const uint32_t p = mine ? sc.par[it.seg_begin + s] : 0u;
+      const uint32_t bal = __ballot_sync(0xffffffffu, (p >> (2 * K)) & 1u);
+      const uint32_t in = bit ^ (__popc(bal & lt) & 1u);  // incoming bit 2K of segment s
+      if (mine && in) {
+        const uint32_t hi = (sc.alt[it.seg_begin + s] >> (2 * K + 1)) & 1u;
+        sc.par[it.seg_begin + s] = static_cast<uint8_t>((p & ~(1u << (2 * K + 1))) | (hi << (2 * K + 1)));
+      }
+      bit ^= __popc(bal) & 1u;
+    }
   }
 }
 
@@ -485,9 +595,10 @@ int sm_count(int device) {
   return cache[size_t(device)];
 }
 
-template <int I>
-void launch_pass(uint32_t grid, cudaStream_t s, const HashBatch& b, Scratch sc) {
-  lzk_fnv_pass_kernel<I><<<grid, kBigThreads, 0, s>>>(b, sc);
+template <int K>
+void launch_dual(uint32_t grid, uint32_t rgrid, cudaStream_t s, const HashBatch& b, Scratch sc) {
+  lzk_fnv_dual_pass_kernel<K><<<grid, kBigThreads, 0, s>>>(b, sc);
+  lzk_fnv_resolve_kernel<K><<<rgrid, 256, 0, s>>>(b, sc);
 }
 
 void set_pool_threshold(int device) {
@@ -548,7 +659,7 @@ int launch_hash(cudaStream_t stream, int device, const lzk_hash_desc* d, uint32_
   // stream-ordered device block: item table, then (long ranges) per-segment
   // sums and parities
   const uint64_t table = (uint64_t(n) * sizeof(HashItem) + 255) & ~uint64_t(255);
-  const uint64_t bytes = table + (any_long ? uint64_t(segs) * 9 + 16 : 0);
+  const uint64_t bytes = table + (any_long ? uint64_t(segs) * 10 + 16 : 0);
   void* dev = nullptr;
   LZK_CK(cudaMallocAsync(&dev, bytes, stream));
   uint32_t launches = 0;
@@ -562,11 +673,12 @@ int launch_hash(cudaStream_t stream, int device, const lzk_hash_desc* d, uint32_
     ++launches;
   }
   HashBatch batch{static_cast<const HashItem*>(dev), n, 0, segs, 0};
-  Scratch sc{nullptr, nullptr};
+  Scratch sc{nullptr, nullptr, nullptr};
   if (any_long) {
     sc.S = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(dev) + table);
     sc.par = reinterpret_cast<uint8_t*>(sc.S + segs);
-    const cudaError_t me = cudaMemsetAsync(sc.par, 0, segs, stream);
+    sc.alt = sc.par + segs;
+    const cudaError_t me = cudaMemsetAsync(sc.par, 0, 2 * uint64_t(segs), stream);
     if (me != cudaSuccess) {
       cudaFreeAsync(dev, stream);
       return cuda_fail(me, "fnv: scratch memset");
@@ -578,14 +690,11 @@ int launch_hash(cudaStream_t stream, int device, const lzk_hash_desc* d, uint32_
   const uint32_t small_grid =
       std::max(1u, std::min<uint32_t>((segs + small_warps - 1) / small_warps, ctas * kSmallPerBig));
   if (any_long) {
-    launch_pass<0>(grid, stream, batch, sc);
-    launch_pass<1>(grid, stream, batch, sc);
-    launch_pass<2>(grid, stream, batch, sc);
-    launch_pass<3>(grid, stream, batch, sc);
-    launch_pass<4>(grid, stream, batch, sc);
-    launch_pass<5>(grid, stream, batch, sc);
-    launch_pass<6>(grid, stream, batch, sc);
-    launch_pass<7>(grid, stream, batch, sc);
+    const uint32_t rgrid = (n + 7) / 8;  // resolve: one warp per range
+    launch_dual<0>(grid, rgrid, stream, batch, sc);
+    launch_dual<1>(grid, rgrid, stream, batch, sc);
+    launch_dual<2>(grid, rgrid, stream, batch, sc);
+    launch_dual<3>(grid, rgrid, stream, batch, sc);
     launches += 8;
   }
   if (any_long) {

@@ -174,3 +174,87 @@ if __name__ == "__main__":
         h0 = rng.getrandbits(64)
         assert segmented(d, h0, sl) == fnv(d, h0), (n, sl)
     print("segmented ok")
+
+
+def dual_chunk(chunk, carry, K):
+    """Bit-sliced model of scan_dual<K> (one 1 KiB window): planes 0..2K with
+    the carry-ins in `carry`, then plane 2K+1's parity for x_{2K} and for its
+    complement (incoming bit 2K = 0 / 1). Returns (carry, alt_parity)."""
+    nl = 32
+    Bs = [planes_of(chunk[32 * j:32 * j + 32]) for j in range(nl)]
+    X = [[0] * 8 for _ in range(nl)]
+    carry = list(carry)
+
+    def pref(e):
+        p = e
+        for sh in (1, 2, 4, 8, 16):
+            p ^= (p << sh) & 0xFFFFFFFF
+        return p
+
+    for i in range(2 * K + 1):
+        ps = [pref(plane_e(i, Bs[j], X[j])) for j in range(nl)]
+        bal = sum(((ps[j] >> 31) & 1) << j for j in range(nl))
+        for j in range(nl):
+            cin = (bin(bal & ((1 << j) - 1)).count("1") + carry[i]) & 1
+            X[j][i] = ((ps[j] << 1) & 0xFFFFFFFF) ^ (0xFFFFFFFF if cin else 0) ^ Bs[j][i]
+        carry[i] ^= bin(bal).count("1") & 1
+    alt = 0
+    for hyp in (0, 1):
+        par = 0
+        for j in range(nl):
+            Xh = list(X[j])
+            if hyp:
+                Xh[2 * K] ^= 0xFFFFFFFF
+            par ^= (pref(plane_e(2 * K + 1, Bs[j], Xh)) >> 31) & 1
+        if hyp:
+            alt ^= par
+        else:
+            carry[2 * K + 1] ^= par
+    return carry, alt
+
+
+def segmented_dual(data, h0, seglen):
+    """Four dual passes + resolve (lzk_fnv_dual_pass_kernel /
+    lzk_fnv_resolve_kernel), then the final pass + combine."""
+    assert seglen % 1024 == 0
+    segs = [data[k:k + seglen] for k in range(0, len(data), seglen)] or [b""]
+    l0 = h0 & 0xFF
+    par = [0] * len(segs)
+    alt = [0] * len(segs)
+    for K in range(4):
+        for k, s in enumerate(segs[:-1]):
+            lin = l0
+            for q in par[:k]:
+                lin ^= q
+            cin = lin & ((1 << (2 * K)) - 1)
+            carry = [(cin >> i) & 1 for i in range(8)]
+            a = 0
+            for c in range(0, len(s), 1024):
+                carry, da = dual_chunk(s[c:c + 1024], carry, K)
+                a ^= da
+            par[k] |= (carry[2 * K] << (2 * K)) | (carry[2 * K + 1] << (2 * K + 1))
+            alt[k] |= a << (2 * K + 1)
+        bit = (l0 >> (2 * K)) & 1  # resolve: pick the hypothesis per segment
+        for k in range(len(segs) - 1):
+            if bit:
+                par[k] = (par[k] & ~(1 << (2 * K + 1))) | (alt[k] & (1 << (2 * K + 1)))
+            bit ^= (par[k] >> (2 * K)) & 1
+    h = h0
+    for k, s in enumerate(segs):
+        lin = l0
+        for q in par[:k]:
+            lin ^= q
+        assert lin == h & 0xFF, (k, lin, h & 0xFF)
+        acc = fnv(s, lin)
+        h = (pow(P, len(s), 1 << 64) * h + acc - pow(P, len(s), 1 << 64) * lin) & M64
+    return h
+
+
+if __name__ == "__main__":
+    rng = random.Random(11)
+    for n, sl in ((5 * 1024 + 77, 1024), (8 * 1024, 2048), (3 * 1024, 1024)):
+        for trial in range(3):
+            d = bytes(rng.getrandbits(8) for _ in range(n))
+            h0 = rng.getrandbits(64)
+            assert segmented_dual(d, h0, sl) == fnv(d, h0), (n, sl, trial)
+    print("segmented dual ok")
