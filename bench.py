@@ -453,9 +453,11 @@ def main_ours(args, rank, world, local_rank):
                              "unit": "GB/s", "frac": round(per_gpu / PCIE_GEN5_X16_GBPS, 4),
                              # NVML PCIe TX counter of this GPU over the timed steps, per step
                              "traffic": None if pcie.bytes is None else round(pcie.bytes / args.steps),
-                             "traffic_source": "nvmlDeviceGetPcieThroughput(TX) read on a 20 ms tick over the "
-                                               "timed steps and integrated, per step (includes TLP/protocol "
-                                               "overhead); algorithmic bytes per step = payload",
+                             "traffic_source": "nvmlDeviceGetPcieThroughput(TX) read back to back over the timed "
+                                               "steps and integrated, per step (includes TLP/protocol overhead; "
+                                               "a raw DMA of known size reads 1.12x on this counter, "
+                                               "profiles/r02_pcie_counter_probe.txt); algorithmic bytes per "
+                                               "step = payload",
                              "peak_measured_dma": link["dma_gbps"],
                              "frac_of_measured_dma": round(per_gpu / link["dma_gbps"], 4),
                              "kernel": {"name": "lzk_gather_kernel", "achieved": kernel_gbps,
@@ -516,14 +518,13 @@ class PcieSampler:
         return self
 
     def _run(self):
-        # each reading is the rate over NVML's most recent 20 ms window: read
-        # on a 20 ms tick and weight each reading by the time since the last
-        period = 0.02
+        # A call blocks for one ~20-26 ms NVML sampling window and returns that
+        # window's rate, so back-to-back readings tile the time: weight each
+        # by the time since the previous one (profiles/r02_pcie_counter_probe.txt:
+        # a raw 68.7 GB DMA integrates to 1.12x its bytes this way; a 20 ms
+        # tick with sleeps overcounts, the cumulative field counter wraps)
         last = time.perf_counter()
-        tick = last
         while not self._stop.is_set():
-            tick += period
-            time.sleep(max(0.0, tick - time.perf_counter()))
             kbps = self._nvml.nvmlDeviceGetPcieThroughput(self._h, self._nvml.NVML_PCIE_UTIL_TX_BYTES)
             now = time.perf_counter()
             self.bytes += kbps * 1e3 * (now - last)
