@@ -412,13 +412,13 @@ def main_ours(args, rank, world, local_rank):
             try:
                 sw = W.llama_layer_sample(layers=n_sample if world == 1 else 1, dp=world, rank=rank)
                 sbuilt = lz.build_workload(sw.write_spec(os.path.join(tmp, "sample.spec")), dev)
-                matched, e2e = sample_runs(lz, torch, sbuilt, sw, dev, tmp, world, rank, producer, args)
+                matched, e2e = sample_runs(lz, torch, sbuilt, sw, dev, tmp, world, rank, producer)
                 t_max = max_over_ranks(e2e.pop("seconds"))
                 e2e["per_rank_gbps"] = e2e["value"]
                 e2e["value"] = round(sum_over_ranks(float(e2e["d2h_bytes_per_step"] * e2e["steps"])) / t_max / 1e9, 3)
                 e2e["d2h_bytes_per_step"] = int(sum_over_ranks(float(e2e["d2h_bytes_per_step"])))
                 if world == 1 and gemm is not None and not args.skip_train:
-                    durable = durable_stall(lz, torch, sbuilt, tmp, dev, gemm, barrier, stall)
+                    durable = durable_stall(lz, torch, sbuilt, tmp, dev, gemm, barrier)
                 del sbuilt
             except Exception as e:
                 e2e = {"error": f"{type(e).__name__}: {e}"}
@@ -727,7 +727,7 @@ def train_stall(lz, torch, eng, plan, tree, gemm, barrier, step0):
             "variant": "hybrid (engine default)", "gemm": "bf16 8192^3 torch.matmul x%d" % gemm.n_mm}
 
 
-def sample_runs(lz, torch, sbuilt, sw, dev, tmp, world, rank, producer, args):
+def sample_runs(lz, torch, sbuilt, sw, dev, tmp, world, rank, producer):
     """Our engine on the SAME bounded sample the reference arm checkpoints
     (matched pair), durable files (fsync, O_DIRECT interior), and e2e: the
     public API from capture to files durable on local disk, then the
@@ -809,7 +809,7 @@ def sample_runs(lz, torch, sbuilt, sw, dev, tmp, world, rank, producer, args):
     return matched, e2e
 
 
-def durable_stall(lz, torch, sbuilt, tmp, dev, gemm, barrier, stall):
+def durable_stall(lz, torch, sbuilt, tmp, dev, gemm, barrier):
     """Every-iteration checkpoints into real files (fsync, O_DIRECT) with the
     pinned pool smaller than two checkpoints, so the flush backs up into
     capture() as in the reference's trainer loop (bench.cpp:261-313;
