@@ -121,11 +121,14 @@ def load_workloads():
 
 
 def fits_host(bytes_per_rank: int, world: int) -> bool:
+    """Whether `world` pinned rings of `bytes_per_rank` fit this host. Based on
+    MemTotal, not MemAvailable: both arms (and every rank) must derive the same
+    workload, whatever the other processes have allocated by then."""
     try:
-        avail = next(int(l.split()[1]) * 1024 for l in open("/proc/meminfo") if l.startswith("MemAvailable"))
+        total = next(int(l.split()[1]) * 1024 for l in open("/proc/meminfo") if l.startswith("MemTotal"))
     except (OSError, StopIteration):
         return True
-    return bytes_per_rank * world <= 0.75 * avail
+    return bytes_per_rank * world <= 0.70 * total
 
 
 def headline_layers(requested: int, world: int) -> int:
@@ -302,7 +305,7 @@ def main_ours(args, rank, world, local_rank):
             f"{len(w.leaves)} tensors built in {time.time() - t0:.1f} s")
 
         barrier()  # every rank probes its link at the same time (shared uplinks show up)
-        link = measure_link_ceiling(lz, dev)
+        link = measure_link_ceiling(lz, dev, barrier)
         link["numa_node"] = lz.device_numa_node(dev)
         links = gather(link)
         log(f"[bench] rank {rank}: concurrent host-link ceiling: DMA {link['dma_gbps']} GB/s, "
@@ -561,7 +564,7 @@ def measure_streaming(lz, built, plan, payload, tmp, dev, barrier, producer, poo
                     % (payload / 1e9)}
 
 
-def measure_link_ceiling(lz, dev, nbytes=8 << 30, chunk=256 << 20):
+def measure_link_ceiling(lz, dev, barrier=None, nbytes=8 << 30, chunk=256 << 20):
     """Raw ceilings of this box's host link, in this process, with the pool's
     memory kind (THP-registered pinned): back-to-back copy-engine DMAs of
     `chunk` bytes, and plain SM 16-byte stores via the gather kernel over
@@ -591,6 +594,8 @@ def measure_link_ceiling(lz, dev, nbytes=8 << 30, chunk=256 << 20):
             best = 0.0
             ck(fn())  # untimed pass: first-use costs (IOMMU/TLB warm-up) stay out of the probe
             ck(d.lzk_stream_sync(s))
+            if barrier is not None:
+                barrier()  # every rank probes the same variant at the same time
             for _ in range(6):
                 ck(d.lzk_event_record(e0, s))
                 ck(fn())
