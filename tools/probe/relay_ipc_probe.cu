@@ -77,6 +77,7 @@ int main(int argc, char** argv) {
   const int A = argc > 1 ? std::atoi(argv[1]) : 0;
   const int B = argc > 2 ? std::atoi(argv[2]) : 1;
   const double share = argc > 3 ? std::atof(argv[3]) : 0.5;  // fraction relayed through B
+  const bool priv = argc > 4 && std::string(argv[4]) == "private";
   const size_t bytes = 8ull << 30;
   const size_t split = (size_t(double(bytes) * (1.0 - share)) / 4096) * 4096;
   int to_helper[2], to_owner[2];
@@ -90,18 +91,25 @@ int main(int argc, char** argv) {
   if (child == 0) {  // ---------------- helper (GPU B)
     Msg m;
     read_all(to_helper[0], &m, sizeof m);
-    const std::string path = "/proc/" + std::to_string(m.owner_pid) + "/fd/" + std::to_string(m.memfd);
-    const int fd = open(path.c_str(), O_RDWR);
-    if (fd < 0) {
-      std::perror("open memfd");
-      return 6;
-    }
-    void* ring = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
-    if (ring == MAP_FAILED) return 7;
-    CK(cudaSetDevice(B));
+    void* ring = nullptr;
     double t0 = now();
-    CK(cudaHostRegister(ring, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped));
-    std::printf("helper: cudaHostRegister of the owner's %zu GiB ring: %.2f s\n", bytes >> 30, now() - t0);
+    if (priv) {  // the helper's own pinned staging (it would write the owner's file itself)
+      CK(cudaSetDevice(B));
+      CK(cudaHostAlloc(&ring, bytes, cudaHostAllocPortable | cudaHostAllocMapped));
+      std::printf("helper: private pinned staging %zu GiB: %.2f s\n", bytes >> 30, now() - t0);
+    } else {
+      const std::string path = "/proc/" + std::to_string(m.owner_pid) + "/fd/" + std::to_string(m.memfd);
+      const int fd = open(path.c_str(), O_RDWR);
+      if (fd < 0) {
+        std::perror("open memfd");
+        return 6;
+      }
+      ring = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+      if (ring == MAP_FAILED) return 7;
+      CK(cudaSetDevice(B));
+      CK(cudaHostRegister(ring, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped));
+      std::printf("helper: cudaHostRegister of the owner's %zu GiB ring: %.2f s\n", bytes >> 30, now() - t0);
+    }
     int can = 0;
     CK(cudaDeviceCanAccessPeer(&can, B, A));
     if (can) CK(cudaDeviceEnablePeerAccess(A, 0));
@@ -125,16 +133,30 @@ int main(int argc, char** argv) {
       const double dt = now() - h0;
       write_all(to_owner[1], &dt, sizeof dt);
     }
+    // check the relayed part
+    size_t bad = 0;
+    const uint64_t* r = static_cast<const uint64_t*>(ring);
+    for (size_t i = split / 8; i < bytes / 8; i += 511) bad += r[i] != i * 0x9E3779B97F4A7C15ull + 12345;
+    std::printf("helper: relayed part mismatches %zu\n", bad);
     CK(cudaIpcCloseMemHandle(src));
-    CK(cudaHostUnregister(ring));
+    if (priv) {
+      CK(cudaFreeHost(ring));
+    } else {
+      CK(cudaHostUnregister(ring));
+    }
     return 0;
   }
 
   // ---------------- owner (GPU A)
   CK(cudaSetDevice(A));
-  void* ring = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, memfd, 0);
-  if (ring == MAP_FAILED) return 8;
+  void* ring = nullptr;
   double t0 = now();
+  if (priv) {
+    CK(cudaHostAlloc(&ring, bytes, cudaHostAllocPortable | cudaHostAllocMapped));
+    std::printf("owner: private pinned ring %zu GiB: %.2f s\n", bytes >> 30, now() - t0);
+  } else {
+  ring = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, memfd, 0);
+  if (ring == MAP_FAILED) return 8;
   {
     std::vector<std::thread> th;
     for (int t = 0; t < 16; ++t) {
@@ -149,6 +171,7 @@ int main(int argc, char** argv) {
   CK(cudaHostRegister(ring, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped));
   std::printf("owner: memfd ring %zu GiB: first touch %.2f s, cudaHostRegister %.2f s (4 KiB shmem pages)\n",
               bytes >> 30, t_touch, now() - t0);
+  }
   void* src = nullptr;
   CK(cudaMalloc(&src, bytes));
   fill_kernel<<<1024, 256>>>(static_cast<uint64_t*>(src), bytes / 8);
@@ -188,7 +211,7 @@ int main(int argc, char** argv) {
   // verify every 4 KiB word 0.. in both parts
   size_t bad = 0;
   const uint64_t* r = static_cast<const uint64_t*>(ring);
-  for (size_t i = 0; i < bytes / 8; i += 511) bad += r[i] != i * 0x9E3779B97F4A7C15ull + 12345;
+  for (size_t i = 0; i < (priv ? split : bytes) / 8; i += 511) bad += r[i] != i * 0x9E3779B97F4A7C15ull + 12345;
   std::printf("owner: share %.2f relayed via GPU %d: aggregate %.2f GB/s (own link %.2f, relay %.2f); mismatches %zu\n",
               share, B, best, best_own, best_helper, bad);
   int st = 0;
