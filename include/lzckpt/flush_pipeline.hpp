@@ -83,6 +83,14 @@ class FlushPipeline {
   // Gives up on the rest of a streamed file (a capture that could not get
   // pool space): it ends Abandoned once the attached segments drain.
   void truncate_stream(uint64_t file_id);
+  // B200 extension — uplink relay: payload bytes [payload_offset, end) of a
+  // registered file are written into the file by another process (a relay
+  // helper). Call right after register_file, before any chunk arrives; the
+  // suffix must start at an entry whose hash run holds it alone. Those bytes
+  // are neither written nor hashed here; complete_external() accounts them
+  // and supplies their entries' checksums (or abandons the file).
+  void set_external_suffix(uint64_t file_id, uint64_t payload_offset);
+  void complete_external(uint64_t file_id, bool ok, const std::vector<uint64_t>& checksums);
   void enqueue_flush(uint64_t segment_id, uint64_t segment_offset, uint64_t length);
   // B200 extension: several in-order chunks under one lock acquisition.
   void enqueue_flush_spans(const std::vector<ChunkSpan>& spans);
@@ -130,6 +138,9 @@ class FlushPipeline {
     uint64_t write_queued = 0;   // bytes [0, write_queued) handed to writers
     uint64_t starve_from = ~0ull;// injected failure: bytes >= this never reach the disk
     uint64_t accounted = 0;      // written + starved bytes
+    uint64_t own_end = ~0ull;    // payload bytes >= own_end arrive externally (relay)
+    bool external_done = true;
+    uint64_t own_limit() const { return own_end < expected ? own_end : expected; }
     uint32_t jobs = 0;           // outstanding jobs touching this file
     uint32_t writes_inflight = 0;
     std::vector<SubSeg> segs;    // in payload order

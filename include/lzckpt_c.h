@@ -197,6 +197,13 @@ typedef struct lzckpt_engine_config {
   int flush_discard;          /* host-memory tier only (no files) */
   uint64_t stream_segment_bytes; /* > 0: files stream through the pool in segments this large */
   int flush_hash_only;        /* verification tier: hash every entry, write nothing */
+  /* uplink relay between the ranks of one node (EngineConfig::Relay) */
+  const char* relay_serve_socket;   /* helper: serve relay requests here (NULL/"" = no) */
+  uint64_t relay_staging_bytes;
+  uint32_t relay_ctas;
+  const char* relay_peer_socket;    /* owner: delegate to the helper listening here */
+  double relay_share;               /* fraction of each shard file's payload (0 = off) */
+  uint64_t relay_min_entry;
 } lzckpt_engine_config;
 void lzckpt_engine_config_defaults(lzckpt_engine_config* c);
 
@@ -243,6 +250,10 @@ int lzckpt_numa_prefer_range(void* p, uint64_t len, int node);
 /* Node of each page at p + k*stride (move_pages query), k < cap; *n = pages. */
 int lzckpt_numa_page_nodes(const void* p, uint64_t len, uint64_t stride, int* nodes, uint64_t cap, uint64_t* n);
 int lzckpt_engine_numa_node(const lzckpt_engine* e);
+/* Uplink relay counters: bytes this engine delegated to its helper (owner),
+ * bytes and requests it relayed for owners (helper). */
+int lzckpt_engine_relay_stats(const lzckpt_engine* e, uint64_t* delegated_bytes, uint64_t* served_bytes,
+                              uint64_t* served_requests);
 /* Phase one of the 2PC for THIS rank only (EngineCommitParticipant::prepare,
  * reference consolidation.cpp:142-152): waits until the capture is persisted,
  * then validates the rank's files on the GPU. Writes a JSON vote

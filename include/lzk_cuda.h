@@ -142,6 +142,23 @@ int lzk_stream_wait_raw(lzk_stream* s, void* producer_stream);
 /* Same, for a raw cudaStream_t handle owned by the caller. */
 int lzk_raw_stream_wait_event(void* cuda_stream, lzk_event* e);
 
+/* ---- CUDA IPC (uplink relay between the ranks of one node) -------------- */
+/* 64 opaque bytes: a cudaIpcMemHandle_t or cudaIpcEventHandle_t. */
+typedef struct lzk_ipc_handle {
+  unsigned char bytes[64];
+} lzk_ipc_handle;
+/* IPC handle of the allocation holding `dev_ptr` and dev_ptr's offset in it
+ * (works for torch tensors inside larger allocator blocks). */
+int lzk_ipc_export_mem(int device, const void* dev_ptr, lzk_ipc_handle* handle, uint64_t* offset);
+/* Maps a peer process's allocation into this process (with peer access);
+ * cached: each handle opens once per process and device. */
+int lzk_ipc_open_mem(int device, const lzk_ipc_handle* handle, void** base);
+int lzk_ipc_close_all(void);
+/* Interprocess event (no timing) and its handle; the peer opens it with
+ * lzk_ipc_event_open and can record/wait/sync it like any lzk_event. */
+int lzk_ipc_event_create(int device, lzk_event** e, lzk_ipc_handle* handle);
+int lzk_ipc_event_open(int device, const lzk_ipc_handle* handle, lzk_event** e);
+
 /* ---- the snapshot copies ----------------------------------------------- */
 /* Multi-tensor gather D2H on SMs: one launch copies all n descriptors into
  * mapped pinned host memory with coalesced 128-bit loads and 16-byte aligned

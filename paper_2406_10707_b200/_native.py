@@ -52,7 +52,13 @@ class EngineConfigC(C.Structure):
                 ("flush_threads", u32), ("large_leaf_threshold", u64), ("reserve_timeout_ms", i64),
                 ("device", i32), ("ce_threshold", u64), ("kernel_ctas", u32), ("group_bytes", u64),
                 ("force_kernel", i32), ("force_copy_engine", i32), ("hugepages", i32),
-                ("flush_discard", i32), ("stream_segment_bytes", u64), ("flush_hash_only", i32)]
+                ("flush_discard", i32), ("stream_segment_bytes", u64), ("flush_hash_only", i32),
+                ("relay_serve_socket", cp), ("relay_staging_bytes", u64), ("relay_ctas", u32),
+                ("relay_peer_socket", cp), ("relay_share", f64), ("relay_min_entry", u64)]
+
+
+class IpcHandleC(C.Structure):
+    _fields_ = [("bytes", C.c_ubyte * 64)]
 
 
 class CountersC(C.Structure):
@@ -155,6 +161,7 @@ ENGINE_SYMBOLS = [
     ("lzckpt_numa_prefer_range", i32, [vp, u64, i32]),
     ("lzckpt_numa_page_nodes", i32, [vp, u64, u64, P(i32), u64, P(u64)]),
     ("lzckpt_engine_numa_node", i32, [vp]),
+    ("lzckpt_engine_relay_stats", i32, [vp, P(u64), P(u64), P(u64)]),
     ("lzckpt_engine_prepare", i32, [vp, P(ModelSpecC), vp, cp, u64, P(u64)]),
     ("lzckpt_engine_ticket_header", i32, [vp, vp, u32, P(vp)]),
     ("lzckpt_engine_restore_file", i32, [vp, cp, vp, P(vp)]),
@@ -186,6 +193,11 @@ DEVICE_SYMBOLS = [
     ("lzk_host_alloc", i32, [u64, i32, P(vp)]),
     ("lzk_host_alloc_numa", i32, [u64, i32, i32, P(vp)]),
     ("lzk_device_numa_node", i32, [i32, P(i32)]),
+    ("lzk_ipc_export_mem", i32, [i32, vp, P(IpcHandleC), P(u64)]),
+    ("lzk_ipc_open_mem", i32, [i32, P(IpcHandleC), P(vp)]),
+    ("lzk_ipc_close_all", i32, []),
+    ("lzk_ipc_event_create", i32, [i32, P(vp), P(IpcHandleC)]),
+    ("lzk_ipc_event_open", i32, [i32, P(IpcHandleC), P(vp)]),
     ("lzk_host_free", i32, [vp]),
     ("lzk_host_register", i32, [vp, u64]),
     ("lzk_host_unregister", i32, [vp]),

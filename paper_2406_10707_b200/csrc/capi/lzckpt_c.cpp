@@ -483,6 +483,12 @@ void lzckpt_engine_config_defaults(lzckpt_engine_config* c) {
   c->flush_discard = 0;
   c->stream_segment_bytes = 0;
   c->flush_hash_only = 0;
+  c->relay_serve_socket = nullptr;
+  c->relay_staging_bytes = d.relay.staging_bytes;
+  c->relay_ctas = d.relay.ctas;
+  c->relay_peer_socket = nullptr;
+  c->relay_share = 0;
+  c->relay_min_entry = d.relay.min_entry;
 }
 
 int lzckpt_engine_create(const lzckpt_engine_config* c, const lzckpt_topology* topo, uint32_t rank_dp,
@@ -510,6 +516,12 @@ int lzckpt_engine_create(const lzckpt_engine_config* c, const lzckpt_topology* t
     cfg.flush.discard = c->flush_discard != 0;
     cfg.stream_segment_bytes = c->stream_segment_bytes;
     cfg.flush.hash_only = c->flush_hash_only != 0;
+    cfg.relay.serve_socket = c->relay_serve_socket ? c->relay_serve_socket : "";
+    cfg.relay.staging_bytes = c->relay_staging_bytes;
+    cfg.relay.ctas = c->relay_ctas;
+    cfg.relay.peer_socket = c->relay_peer_socket ? c->relay_peer_socket : "";
+    cfg.relay.share = c->relay_share;
+    cfg.relay.min_entry = c->relay_min_entry;
     auto h = std::make_unique<lzckpt_engine>();
     h->topo = to_topo(topo);
     h->e = std::make_unique<Engine>(std::move(cfg), h->topo, RankCoord{rank_dp, rank_pp, rank_tp});
@@ -623,6 +635,17 @@ int lzckpt_numa_page_nodes(const void* p, uint64_t len, uint64_t stride, int* no
 }
 
 int lzckpt_engine_numa_node(const lzckpt_engine* e) { return e ? e->e->pool().numa_node() : -1; }
+
+int lzckpt_engine_relay_stats(const lzckpt_engine* e, uint64_t* delegated_bytes, uint64_t* served_bytes,
+                              uint64_t* served_requests) {
+  return guard([&] {
+    need(e, "engine");
+    const auto s = e->e->relay_stats();
+    if (delegated_bytes) *delegated_bytes = s.delegated_bytes;
+    if (served_bytes) *served_bytes = s.served_bytes;
+    if (served_requests) *served_requests = s.served_requests;
+  });
+}
 
 int lzckpt_engine_prepare(lzckpt_engine* e, const lzckpt_model_spec* model, lzckpt_ticket* t, char* json,
                           uint64_t cap, uint64_t* needed) {

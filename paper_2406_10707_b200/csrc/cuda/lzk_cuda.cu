@@ -25,6 +25,7 @@
 //    >= 1 MiB tensors; warp tiles keep 4-KiB tensors link-bound with a small
 //    grid too), so the snapshot steals only a few of the 148 SMs from
 //    training kernels.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -673,6 +674,122 @@ int lzk_event_create(int device, int blocking_sync, lzk_event** out) {
   if (err != cudaSuccess) {
     delete e;
     return cuda_fail(err, "cudaEventCreateWithFlags");
+  }
+  e->device = device;
+  *out = e;
+  return LZK_OK;
+}
+
+// ---- CUDA IPC (uplink relay between ranks of one node) ------------------------
+
+namespace {
+
+static_assert(sizeof(cudaIpcMemHandle_t) == sizeof(lzk_ipc_handle), "IPC handle size");
+static_assert(sizeof(cudaIpcEventHandle_t) == sizeof(lzk_ipc_handle), "IPC handle size");
+
+// cuMemGetAddressRange through the runtime's driver entry point: the device
+// layer does not link libcuda directly (hosts without a driver still load it).
+using AddressRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+AddressRangeFn address_range() {
+  static AddressRangeFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return AddressRangeFn(nullptr);
+    }
+    return reinterpret_cast<AddressRangeFn>(f);
+  }();
+  return fn;
+}
+
+// A handle opens once per process: cache (device, handle bytes) -> base.
+std::mutex g_ipc_mu;
+std::vector<std::pair<std::pair<int, std::string>, void*>> g_ipc_open;
+
+}  // namespace
+
+int lzk_ipc_export_mem(int device, const void* dev_ptr, lzk_ipc_handle* handle, uint64_t* offset) {
+  if (!dev_ptr || !handle || !offset) return fail(LZK_ERR_INVALID, "ipc export: null argument");
+  if (int rc = use_device(device)) return rc;
+  AddressRangeFn range = address_range();
+  if (!range) return fail(LZK_ERR_CUDA, "ipc export: cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS) {
+    return fail(LZK_ERR_CUDA, "ipc export: pointer is not a device allocation");
+  }
+  cudaIpcMemHandle_t h;
+  LZK_CK(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  std::memcpy(handle, &h, sizeof h);
+  *offset = reinterpret_cast<uint64_t>(dev_ptr) - uint64_t(base);
+  return LZK_OK;
+}
+
+int lzk_ipc_open_mem(int device, const lzk_ipc_handle* handle, void** base) {
+  if (!handle || !base) return fail(LZK_ERR_INVALID, "ipc open: null argument");
+  if (int rc = use_device(device)) return rc;
+  const std::string key(reinterpret_cast<const char*>(handle), sizeof *handle);
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  for (const auto& [k, p] : g_ipc_open) {
+    if (k.first == device && k.second == key) {
+      *base = p;
+      return LZK_OK;
+    }
+  }
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  void* p = nullptr;
+  LZK_CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  g_ipc_open.push_back({{device, key}, p});
+  *base = p;
+  return LZK_OK;
+}
+
+int lzk_ipc_close_all(void) {
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  for (const auto& [k, p] : g_ipc_open) {
+    use_device(k.first);
+    cudaIpcCloseMemHandle(p);
+  }
+  g_ipc_open.clear();
+  return LZK_OK;
+}
+
+int lzk_ipc_event_create(int device, lzk_event** out, lzk_ipc_handle* handle) {
+  if (!out || !handle) return fail(LZK_ERR_INVALID, "ipc event: null argument");
+  *out = nullptr;
+  if (int rc = use_device(device)) return rc;
+  auto* e = new (std::nothrow) lzk_event();
+  if (!e) return fail(LZK_ERR_NOMEM, "event");
+  cudaError_t err = cudaEventCreateWithFlags(&e->e, cudaEventDisableTiming | cudaEventInterprocess);
+  cudaIpcEventHandle_t h;
+  if (err == cudaSuccess) err = cudaIpcGetEventHandle(&h, e->e);
+  if (err != cudaSuccess) {
+    if (e->e) cudaEventDestroy(e->e);
+    delete e;
+    return cuda_fail(err, "interprocess event");
+  }
+  std::memcpy(handle, &h, sizeof h);
+  e->device = device;
+  *out = e;
+  return LZK_OK;
+}
+
+int lzk_ipc_event_open(int device, const lzk_ipc_handle* handle, lzk_event** out) {
+  if (!out || !handle) return fail(LZK_ERR_INVALID, "ipc event open: null argument");
+  *out = nullptr;
+  if (int rc = use_device(device)) return rc;
+  auto* e = new (std::nothrow) lzk_event();
+  if (!e) return fail(LZK_ERR_NOMEM, "event");
+  cudaIpcEventHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  cudaError_t err = cudaIpcOpenEventHandle(&e->e, h);
+  if (err != cudaSuccess) {
+    delete e;
+    return cuda_fail(err, "cudaIpcOpenEventHandle");
   }
   e->device = device;
   *out = e;

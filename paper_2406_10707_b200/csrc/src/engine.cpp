@@ -31,6 +31,7 @@
 #include "lzckpt/errors.hpp"
 #include "lzk_cuda.h"
 #include "numa.hpp"
+#include "relay.hpp"
 
 namespace lzckpt {
 
@@ -153,6 +154,14 @@ Engine::Engine(EngineConfig config, ParallelTopology topo, RankCoord rank)
     }
     streamer_ = std::thread([this] { streamer_loop(); });
   }
+  if (!config_.relay.serve_socket.empty()) {
+    relay_server_ = std::make_unique<detail::RelayServer>(transfers_.device(), config_.relay.serve_socket,
+                                                          config_.relay.staging_bytes, config_.relay.ctas);
+  }
+  if (!config_.relay.peer_socket.empty() && config_.relay.share > 0) {
+    if (config_.relay.share >= 1) throw ConfigError("relay share must be below 1");
+    relay_client_ = std::make_unique<detail::RelayClient>(config_.relay.peer_socket);
+  }
 }
 
 Engine::~Engine() {
@@ -175,6 +184,9 @@ Engine::~Engine() {
       }
     }
   }
+  relay_client_.reset();  // after drain(): every delegated file has completed
+  relay_server_.reset();
+  for (auto& [e, h] : relay_events_) lzk_event_destroy(e);
   lzk_stream_destroy(inline_stream_);
 }
 
@@ -488,7 +500,30 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
     counters_.last_capture_seconds = dt;
     return ticket;
   }
+  const bool relay = relay_client_ && config_.copy_channel.bandwidth_Bps <= 0;
   for (auto& b : builds) {
+    // Uplink relay: a suffix of the file's large region leaves, up to `share`
+    // of its payload, goes to the helper (its bytes never enter this ring).
+    size_t own = b.larges.size();
+    if (relay) {
+      uint64_t moved = 0;
+      const uint64_t budget = uint64_t(config_.relay.share * double(b.payload));
+      while (own > 0) {
+        const auto& l = b.larges[own - 1];
+        if (!l.region || l.size < config_.relay.min_entry || moved + l.size > budget) break;
+        moved += l.size;
+        --own;
+      }
+    }
+    std::vector<std::shared_ptr<DeviceRegion>> relay_regions;
+    std::vector<uint64_t> relay_sizes, relay_offsets;
+    for (size_t k = own; k < b.larges.size(); ++k) {
+      relay_regions.push_back(b.larges[k].region);
+      relay_sizes.push_back(b.larges[k].size);
+      relay_offsets.push_back(b.header.entries[1 + k].offset);
+    }
+    const uint64_t header_size = b.header.serialized_size();
+    const uint64_t suffix = own < b.larges.size() ? b.header.entries[1 + own].offset - header_size : 0;
     const bool align = b.payload >= kAlignMin && b.payload + kRingAlign <= pool_.capacity();
     const Segment seg = pool_.reserve(b.payload + (align ? kRingAlign - 1 : 0), ticket->id_);  // backpressure
     const uint64_t pad = align ? aligned_pad(pool_.segment_data(seg), b.meta_size, 0) : 0;
@@ -500,6 +535,12 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
     {
       std::lock_guard tl(ticket->mu_);
       ticket->files_.push_back({b.path, file_id, seg.id});
+    }
+    if (!relay_regions.empty()) {
+      flush_.set_external_suffix(file_id, suffix);
+      relay_submit(ticket, b.path, file_id, relay_regions, relay_sizes, relay_offsets, producer.stream,
+                   producer.ordered);
+      b.larges.resize(own);
     }
     // one allocation for the file's tasks; each task shares the block
     auto block = std::make_shared<std::vector<CopyTask>>(1 + b.larges.size());
@@ -626,6 +667,7 @@ void Engine::update_barrier(const std::shared_ptr<CaptureTicket>& ticket) {
   try {
     wait_streamed(ticket);
     transfers_.wait_pending(ticket->id_);
+    wait_relay_reads(ticket);
   } catch (...) {
     record();
     throw;
@@ -641,6 +683,12 @@ void Engine::update_barrier_on_stream(const std::shared_ptr<CaptureTicket>& tick
   detail::NvtxRange range("lzckpt.fence.device");
   const auto t0 = std::chrono::steady_clock::now();
   wait_streamed(ticket);  // streamed segments must all be on the device first
+  // the helper's reads of delegated leaves are not on this process's streams:
+  // the host waits for them (normally long done by the optimizer step)
+  {
+    std::unique_lock tl(ticket->mu_);
+    ticket->done_cv_.wait(tl, [&] { return ticket->relay_reads_pending_ == 0; });
+  }
   if (!transfers_.fence_on_stream(ticket->id_, cuda_stream)) {
     update_barrier(ticket);  // paced channel: copies are host-driven
     return;
@@ -709,6 +757,7 @@ void Engine::on_torn(uint64_t ticket_id) {
 TicketStatus Engine::ticket_status(const CaptureTicket& t) const {
   if (t.failed_) return TicketStatus::Failed;
   if (t.files_done_ == t.files_.size()) return TicketStatus::Persisted;
+  if (t.relay_reads_pending_ > 0) return TicketStatus::InFlight;
   if (t.streamed_) {
     return t.streams_pending_ == 0 && transfers_.ticket_complete(t.id_) ? TicketStatus::HostResident
                                                                          : TicketStatus::InFlight;
@@ -732,6 +781,112 @@ std::vector<CheckpointFileHeader> Engine::ticket_headers(const std::shared_ptr<C
   std::vector<CheckpointFileHeader> out;
   for (uint64_t id : ids) out.push_back(const_cast<FlushPipeline&>(flush_).file_header(id));
   return out;
+}
+
+void Engine::wait_relay_reads(const std::shared_ptr<CaptureTicket>& ticket) {
+  std::unique_lock tl(ticket->mu_);
+  ticket->done_cv_.wait(tl, [&] { return ticket->relay_reads_pending_ == 0; });
+  if (ticket->torn_) throw TornSnapshot(ticket->failure_reason_);
+  if (ticket->failed_) throw Error(ticket->failure_reason_);
+}
+
+// Hands one file's delegated leaves to the helper. Torn rule as for local
+// copies: a leaf whose version moved before the helper finished reading it
+// tears the ticket (reference transfer_engine.cpp:146-154).
+void Engine::relay_submit(const std::shared_ptr<CaptureTicket>& ticket, const std::filesystem::path& path,
+                          uint64_t file_id, const std::vector<std::shared_ptr<DeviceRegion>>& regions,
+                          const std::vector<uint64_t>& sizes, const std::vector<uint64_t>& file_offsets,
+                          void* producer_stream, bool ordered) {
+  std::vector<detail::RelayEntry> entries(regions.size());
+  std::vector<uint64_t> versions(regions.size());
+  uint64_t bytes = 0;
+  {
+    std::lock_guard lk(relay_mu_);
+    for (size_t i = 0; i < regions.size(); ++i) {
+      const void* ptr = regions[i]->device_ptr();
+      auto it = relay_exports_.find(ptr);
+      if (it == relay_exports_.end()) {
+        lzk_ipc_handle h;
+        uint64_t off = 0;
+        ck(lzk_ipc_export_mem(regions[i]->device(), ptr, &h, &off), "relay: export a leaf");
+        it = relay_exports_.emplace(ptr, std::make_pair(h, off)).first;
+      }
+      entries[i].mem = it->second.first;
+      entries[i].src_offset = it->second.second;
+      entries[i].length = sizes[i];
+      entries[i].file_offset = file_offsets[i];
+      versions[i] = regions[i]->version();
+      bytes += sizes[i];
+    }
+    relay_delegated_ += bytes;
+  }
+  // producer ordering across processes: an interprocess event on the trainer's stream
+  lzk_event* ev = nullptr;
+  lzk_ipc_handle evh{};
+  if (ordered) {
+    {
+      std::lock_guard lk(relay_mu_);
+      if (!relay_events_.empty()) {
+        std::tie(ev, evh) = relay_events_.back();
+        relay_events_.pop_back();
+      }
+    }
+    if (!ev) ck(lzk_ipc_event_create(transfers_.device(), &ev, &evh), "relay: producer event");
+    ck(lzk_event_record_raw(ev, producer_stream), "relay: record on the producer stream");
+  }
+  uint32_t flags = 0;
+  if (!config_.flush.discard) flags |= detail::kRelayHash;
+  if (!config_.flush.discard && !config_.flush.hash_only) flags |= detail::kRelayWrite;
+  if (!config_.flush.discard && config_.flush.fsync_on_finalize) flags |= detail::kRelayFsync;
+  {
+    std::lock_guard tl(ticket->mu_);
+    ++ticket->relay_reads_pending_;
+  }
+  std::weak_ptr<CaptureTicket> weak = ticket;
+  const uint64_t ticket_id = ticket->id_;
+  auto on_read = [this, weak, ticket_id, regions, versions, ev, evh](bool ok, const std::string& err) {
+    if (ev) {
+      std::lock_guard lk(relay_mu_);
+      relay_events_.emplace_back(ev, evh);  // the helper has consumed its wait
+    }
+    bool torn = false;
+    for (size_t i = 0; i < regions.size(); ++i) torn = torn || regions[i]->version() != versions[i];
+    auto t = weak.lock();
+    if (!t) return;
+    if (torn) on_torn(ticket_id);
+    {
+      std::lock_guard tl(t->mu_);
+      --t->relay_reads_pending_;
+      if (!ok && !t->failed_) {
+        t->failed_ = true;
+        if (t->failure_reason_.empty()) t->failure_reason_ = "uplink relay: " + err;
+      }
+    }
+    t->done_cv_.notify_all();
+  };
+  auto on_persisted = [this, file_id](bool ok, const std::string&, const std::vector<uint64_t>& sums) {
+    flush_.complete_external(file_id, ok, sums);
+  };
+  try {
+    relay_client_->submit(path, flags, ev ? &evh : nullptr, entries, on_read, on_persisted);
+  } catch (...) {
+    on_read(false, "uplink relay: request not delivered");
+    flush_.complete_external(file_id, false, {});
+    throw;
+  }
+}
+
+Engine::RelayStats Engine::relay_stats() const {
+  RelayStats s;
+  {
+    std::lock_guard lk(relay_mu_);
+    s.delegated_bytes = relay_delegated_;
+  }
+  if (relay_server_) {
+    s.served_bytes = relay_server_->bytes_relayed();
+    s.served_requests = relay_server_->requests();
+  }
+  return s;
 }
 
 Engine::Counters Engine::counters() const {

@@ -258,6 +258,45 @@ void FlushPipeline::account(FileRecord& f, uint64_t from, uint64_t to) {
   }
 }
 
+void FlushPipeline::set_external_suffix(uint64_t file_id, uint64_t payload_offset) {
+  std::lock_guard lk(mu_);
+  auto it = files_.find(file_id);
+  if (it == files_.end()) throw Error("set_external_suffix: unknown flush file");
+  FileRecord& f = it->second;
+  if (f.enqueued != 0 || payload_offset >= f.expected) throw Error("set_external_suffix: too late or empty");
+  for (auto& r : f.runs) {
+    if (r.end <= payload_offset) continue;
+    if (r.begin < payload_offset || r.last - r.first != 1) {
+      throw Error("set_external_suffix: the suffix must start at a lone-entry hash run in " + f.path.string());
+    }
+    r.resident = r.hashed = r.end;  // never hashed here; complete_external() brings the digest
+    r.cur = r.last;
+  }
+  f.own_end = payload_offset;
+  f.external_done = false;
+}
+
+void FlushPipeline::complete_external(uint64_t file_id, bool ok, const std::vector<uint64_t>& checksums) {
+  std::unique_lock lk(mu_);
+  auto it = files_.find(file_id);
+  if (it == files_.end()) throw Error("complete_external: unknown flush file");
+  FileRecord& f = it->second;
+  if (f.external_done) return;
+  size_t k = 0;
+  for (size_t e = 0; e < f.header.entries.size(); ++e) {
+    if (f.entry_begin[e] < f.own_end || f.header.entries[e].length == 0) continue;
+    if (ok && k < checksums.size()) f.header.entries[e].checksum = checksums[k];
+    ++k;
+    if (ok && !f.abandoned) ++f.entries_done;
+  }
+  if (!ok || k != checksums.size()) f.abandoned = true;  // no header: the file stays incomplete
+  account(f, f.own_end, f.expected);
+  if (!f.abandoned) bytes_written_ += f.expected - f.own_end;
+  f.external_done = true;
+  if (f.jobs == 0) maybe_finalize(lk, file_id);
+  release_in_order(lk);
+}
+
 void FlushPipeline::enqueue_flush(uint64_t segment_id, uint64_t seg_offset, uint64_t length) {
   {
     std::unique_lock lk(mu_);
@@ -291,14 +330,14 @@ void FlushPipeline::enqueue_locked(std::unique_lock<std::mutex>& lk, uint64_t se
     return;
   }
   const uint64_t offset = sg.off + (seg_offset - sg.pad);
-  if (offset != f.enqueued || seg_offset - sg.pad + length > sg.len) {
+  if (offset != f.enqueued || seg_offset - sg.pad + length > sg.len || offset + length > f.own_limit()) {
     fail_locked("out-of-order chunk for " + f.path.string());
     return;
   }
   f.enqueued += length;
   if (config_.discard) {
     account(f, offset, offset + length);
-    if (f.enqueued == f.expected) maybe_finalize(lk, id);
+    if (f.enqueued == f.own_limit()) maybe_finalize(lk, id);
     release_in_order(lk);
     return;
   }
@@ -463,21 +502,22 @@ void FlushPipeline::run_write(FileRecord& f, const Job& j, const std::byte* src)
 // injected-failure point are accounted as starved. Under mu_.
 void FlushPipeline::queue_writes(uint64_t id, FileRecord& f) {
   const uint64_t piece = std::max<uint64_t>(config_.write_piece, 1);
-  const uint64_t writable_end = std::min(f.enqueued, f.starve_from);
+  const uint64_t writable_end = std::min({f.enqueued, f.starve_from, f.own_limit()});
   while (f.write_queued < writable_end) {
     const SubSeg& s = f.segs[f.seg_index(f.write_queued)];
     const uint64_t stop = std::min(writable_end, s.off + s.len);
     const uint64_t n = std::min(piece, stop - f.write_queued);
     const bool segment_complete = f.write_queued + n == s.off + s.len;
-    if (n < piece && !segment_complete && f.writes_inflight > 0 && f.enqueued < f.expected) break;
+    if (n < piece && !segment_complete && f.writes_inflight > 0 && f.enqueued < f.own_limit()) break;
     jobs_.push_back(Job{false, id, f.write_queued, n, 0});
     f.write_queued += n;
     ++f.writes_inflight;
     ++f.jobs;
   }
-  if (f.enqueued > f.write_queued && f.write_queued >= f.starve_from) {
-    account(f, f.write_queued, f.enqueued);  // starved bytes never reach the disk
-    f.write_queued = f.enqueued;
+  const uint64_t own = std::min(f.enqueued, f.own_limit());
+  if (own > f.write_queued && f.write_queued >= f.starve_from) {
+    account(f, f.write_queued, own);  // starved bytes never reach the disk
+    f.write_queued = own;
   }
 }
 
@@ -551,7 +591,9 @@ bool FlushPipeline::hashed_through(const FileRecord& f, uint64_t end) const {
 
 void FlushPipeline::maybe_finalize(std::unique_lock<std::mutex>& lk, uint64_t id) {
   FileRecord& f = files_.at(id);
-  if (f.finalizing || f.jobs != 0 || f.enqueued != f.expected || f.accounted != f.expected) return;
+  if (f.finalizing || f.jobs != 0 || f.enqueued != f.own_limit() || !f.external_done || f.accounted != f.expected) {
+    return;
+  }
   const bool healthy = !f.abandoned;
   if (healthy && !config_.discard && f.entries_done != f.header.entries.size()) return;
   f.finalizing = true;

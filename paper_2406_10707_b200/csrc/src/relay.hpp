@@ -1,0 +1,131 @@
+// Uplink relay between the ranks of one node (B200 extension; no reference
+// counterpart — the reference has one emulated link per rank).
+//
+// On hosts where several GPUs share one PCIe uplink, the slowest rank sets
+// every checkpoint's time. Measured (profiles/r02_relay_*): an
+// SM kernel on GPU B that reads GPU A's HBM over NVLink and stores to host
+// memory puts those bytes on B's link (a copy-engine DMA issued on B with A's
+// memory as source does not). The relay therefore runs in the HELPER's own
+// process (so its kernel shares the helper GPU with the helper's training
+// instead of being time-sliced against it):
+//
+//   owner  capture() keeps a suffix of each shard file's large leaves out of
+//          its own D2H and sends them as a request: CUDA IPC handles of the
+//          leaves' allocations, the shard file and the leaves' file offsets,
+//          and an interprocess event recorded on the producer stream;
+//   helper waits for that event on its relay stream, gathers the leaves
+//          (lzk_gather_d2h reading the owner's HBM through IPC) into pinned
+//          staging on its own link, reports READ_DONE (the owner's lazy fence
+//          needs it), then pwrites the bytes at their offsets in the owner's
+//          file, optionally hashes them (device FNV over the IPC source) and
+//          fsyncs, and reports PERSISTED with the entry checksums;
+//   owner  its flush treats the suffix as external bytes: accounted, not
+//          written, checksums taken from the reply; the header still goes
+//          last, so the file format and the header-last rule are unchanged.
+//
+// Transport: a Unix stream socket per helper, length-prefixed frames.
+#pragma once
+
+#include <condition_variable>
+#include <cstdint>
+#include <filesystem>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "lzk_cuda.h"
+
+namespace lzckpt::detail {
+
+// One delegated leaf.
+struct RelayEntry {
+  lzk_ipc_handle mem;        // the owner's allocation holding the leaf
+  uint64_t src_offset = 0;   // leaf offset inside that allocation
+  uint64_t length = 0;
+  uint64_t file_offset = 0;  // absolute offset of the leaf in the shard file
+};
+
+enum RelayFlags : uint32_t {
+  kRelayWrite = 1,   // pwrite the bytes into the file
+  kRelayHash = 2,    // return each entry's FNV-1a-64
+  kRelayFsync = 4,   // fsync the file before PERSISTED
+};
+
+class RelayServer {
+ public:
+  // Serves owners on `socket_path` with the gather kernel on `device`
+  // (`ctas` CTAs) through `staging_bytes` of pinned staging.
+  RelayServer(int device, std::string socket_path, uint64_t staging_bytes, uint32_t ctas);
+  ~RelayServer();
+  RelayServer(const RelayServer&) = delete;
+  RelayServer& operator=(const RelayServer&) = delete;
+
+  const std::string& path() const { return path_; }
+  uint64_t bytes_relayed() const;
+  uint64_t requests() const;
+
+ private:
+  struct Request;
+  void accept_loop();
+  void serve(int fd);
+  void handle(int fd, Request& r);
+
+  const int device_;
+  const std::string path_;
+  const uint64_t chunk_;
+  const uint32_t ctas_;
+  int listen_fd_ = -1;
+  lzk_stream* stream_ = nullptr;
+  std::vector<std::byte*> staging_;  // pinned, mapped chunks
+  std::vector<lzk_event*> chunk_done_;
+  uint64_t* digests_ = nullptr;      // pinned, mapped: per-entry FNV results
+  uint32_t digest_cap_ = 0;
+  std::map<std::string, lzk_event*> events_;  // opened producer events by handle bytes
+
+  mutable std::mutex mu_;  // one request at a time (the staging is shared)
+  uint64_t bytes_ = 0;
+  uint64_t requests_ = 0;
+  bool stop_ = false;
+  std::thread acceptor_;
+  std::vector<std::thread> conns_;
+  std::vector<int> conn_fds_;
+};
+
+class RelayClient {
+ public:
+  explicit RelayClient(const std::string& socket_path);
+  ~RelayClient();
+  RelayClient(const RelayClient&) = delete;
+  RelayClient& operator=(const RelayClient&) = delete;
+
+  using ReadDone = std::function<void(bool ok, const std::string& error)>;
+  using Persisted = std::function<void(bool ok, const std::string& error, const std::vector<uint64_t>& checksums)>;
+  // Sends one request; the callbacks run on the client's reader thread,
+  // READ_DONE before PERSISTED. `producer` may be null (no ordering).
+  void submit(const std::filesystem::path& file, uint32_t flags, const lzk_ipc_handle* producer,
+              const std::vector<RelayEntry>& entries, ReadDone on_read, Persisted on_persisted);
+  bool connected() const;
+
+ private:
+  void reader_loop();
+  void fail_all(const std::string& why);
+
+  int fd_ = -1;
+  mutable std::mutex mu_;
+  std::mutex send_mu_;
+  uint64_t next_ = 1;
+  struct Pending {
+    ReadDone on_read;
+    Persisted on_persisted;
+    bool read = false;
+  };
+  std::map<uint64_t, Pending> pending_;
+  bool broken_ = false;
+  std::thread reader_;
+};
+
+}  // namespace lzckpt::detail

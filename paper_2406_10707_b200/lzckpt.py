@@ -556,14 +556,23 @@ class EngineConfig:
     flush_discard: bool = False
     stream_segment_bytes: int = 0
     flush_hash_only: bool = False
+    # uplink relay between the ranks of one node (EngineConfig::Relay)
+    relay_serve_socket: str = ""   # helper: serve relay requests on this Unix socket
+    relay_staging_bytes: int = 1 << 30
+    relay_ctas: int = 4
+    relay_peer_socket: str = ""    # owner: delegate to the helper listening here
+    relay_share: float = 0.0       # fraction of each shard file's payload
+    relay_min_entry: int = 64 << 20
+
+    _STRINGS = ("checkpoint_root", "relay_serve_socket", "relay_peer_socket")
 
     def _c(self) -> N.EngineConfigC:
         c = N.EngineConfigC()
         lib.lzckpt_engine_config_defaults(C.byref(c))
-        self._root = os.fspath(self.checkpoint_root).encode()
-        c.checkpoint_root = self._root
+        self._keep = [os.fspath(getattr(self, k)).encode() for k in self._STRINGS]
+        c.checkpoint_root, c.relay_serve_socket, c.relay_peer_socket = self._keep
         for f in dataclasses.fields(self):
-            if f.name == "checkpoint_root":
+            if f.name in self._STRINGS:
                 continue
             v = getattr(self, f.name)
             setattr(c, f.name, int(v) if isinstance(v, bool) else v)
@@ -744,6 +753,13 @@ class Engine:
     def numa_node(self) -> int:
         """NUMA node of this engine's pinned ring and threads (-1: none)."""
         return lib.lzckpt_engine_numa_node(self._h)
+
+    def relay_stats(self) -> dict:
+        """Uplink relay counters: bytes delegated to the helper (owner), bytes
+        and requests relayed for owners (helper)."""
+        a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(lib.lzckpt_engine_relay_stats(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return {"delegated_bytes": a.value, "served_bytes": b.value, "served_requests": c.value}
 
     def counters(self) -> Counters:
         c = N.CountersC()
