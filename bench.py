@@ -311,10 +311,21 @@ def main_ours(args, rank, world, local_rank):
         log(f"[bench] rank {rank}: concurrent host-link ceiling: DMA {link['dma_gbps']} GB/s, "
             f"SM stores {link['sm_store_gbps']} GB/s, NUMA node {link['numa_node']}")
 
+        # uplink relay: ranks whose concurrent link is much slower hand a share
+        # of their large tensors to a rank with spare link (relay.hpp)
+        relay = relay_plan([l["dma_gbps"] for l in links], args.relay)
+        sock = lambda r: f"/tmp/lzk_relay_{os.environ.get('MASTER_PORT', 'solo')}_{r}.sock"  # noqa: E731
+        helper_of = {o: (h, sh) for o, h, sh in relay["pairs"]}
+        serves = any(h == rank for _, h, _ in relay["pairs"])
         pool_bytes = int(built.bytes * 1.01) + (256 << 20)
         cfg = lz.EngineConfig(checkpoint_root=os.path.join(tmp, "ckpt"), host_buffer_bytes=pool_bytes,
                               large_leaf_threshold=1 << 20, fsync_on_finalize=False, flush_discard=True,
-                              hugepages=True, device=dev)
+                              hugepages=True, device=dev,
+                              relay_serve_socket=sock(rank) if serves else "",
+                              relay_peer_socket=sock(helper_of[rank][0]) if rank in helper_of else "",
+                              relay_share=helper_of[rank][1] if rank in helper_of else 0.0)
+        if relay["pairs"]:
+            log(f"[bench] rank {rank}: uplink relay {relay}")
         t0 = time.time()
         eng = lz.Engine(cfg, built.topo, built.rank)
         log(f"[bench] rank {rank}: pinned {pool_bytes / 1e9:.1f} GB pool in {time.time() - t0:.1f} s")
@@ -388,7 +399,9 @@ def main_ours(args, rank, world, local_rank):
 
         # ---- C4 mode: the same shard streamed through a pool 1/7 its size ----
         streaming = None
+        relay_stats = sum_stats(eng.relay_stats(), sum_over_ranks) if relay["pairs"] else None
         if not args.skip_streaming:
+            barrier()  # a helper must outlive its owners' requests
             eng.close()
             del eng
             try:
@@ -406,6 +419,7 @@ def main_ours(args, rank, world, local_rank):
                 stall = train_stall(lz, torch, eng, plan, built.tree, gemm, barrier, step0=500)
             except Exception as e:
                 stall = {"error": f"{type(e).__name__}: {e}"}
+        barrier()
         eng.close()
         del eng
 
@@ -476,6 +490,7 @@ def main_ours(args, rank, world, local_rank):
                              "link_probes_per_rank": [{k: l[k] for k in ("dma_gbps", "sm_store_gbps", "numa_node")}
                                                       for l in links],
                              "algorithmic_bytes_per_step": payload},
+                "relay": dict(relay, stats=relay_stats) if relay["pairs"] else relay,
                 "stall": None if stall is None else dict(stall, durable=durable),
                 "streaming": streaming,
                 "matched": matched,
@@ -537,6 +552,33 @@ class PcieSampler:
         self._stop.set()
         if self._t:
             self._t.join(timeout=5)
+
+
+def relay_plan(rates, mode):
+    """Uplink relay pairs from the ranks' concurrently probed copy-engine
+    rates: each rank well below the fastest (< 80 %) hands `share` of every
+    shard file's payload to one of the fastest ranks, chosen so that both
+    finish together, (1 - x) / r_owner = (1 + x) / r_helper, damped by 10 %
+    and capped at 0.45. mode: auto | off | force (pair ranks 2k -> 2k+1 at
+    0.3 whatever the rates: exercises the path on symmetric boxes)."""
+    n = len(rates)
+    out = {"mode": mode, "rates_gbps": rates, "pairs": []}
+    if mode == "off" or n < 2:
+        return out
+    if mode == "force":
+        out["pairs"] = [(r, r + 1, 0.3) for r in range(0, n - 1, 2)]
+        return out
+    top = max(rates)
+    owners = sorted((r for r in range(n) if rates[r] < 0.8 * top), key=lambda r: rates[r])
+    helpers = sorted((r for r in range(n) if rates[r] >= 0.9 * top), key=lambda r: -rates[r])
+    for o, h in zip(owners, helpers):
+        x = 0.9 * (rates[h] - rates[o]) / (rates[h] + rates[o])
+        out["pairs"].append((o, h, round(min(0.45, x), 3)))
+    return out
+
+
+def sum_stats(stats, sum_over_ranks):
+    return {k: int(sum_over_ranks(float(v))) for k, v in stats.items()}
 
 
 def measure_streaming(lz, built, plan, payload, tmp, dev, barrier, producer, pool=16 << 30, segment=1 << 30):
@@ -954,6 +996,8 @@ def main():
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--skip-streaming", action="store_true")
     ap.add_argument("--skip-configs2", action="store_true")
+    ap.add_argument("--relay", default="auto", choices=["auto", "off", "force"],
+                    help="uplink relay between ranks (N>1): auto = when the concurrent link probes are uneven")
     args = ap.parse_args()
     if args.warmup < 3:
         log("[bench] warmup raised to 3 (timing rules)")

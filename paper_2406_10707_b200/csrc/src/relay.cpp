@@ -363,7 +363,7 @@ void RelayServer::handle(int fd, Request& r) {
 RelayClient::RelayClient(const std::string& socket_path) {
   const sockaddr_un a = address(socket_path);
   // the helper may still be starting: retry for a while
-  for (int attempt = 0; attempt < 300; ++attempt) {
+  for (int attempt = 0; attempt < 1200; ++attempt) {  // 120 s
     fd_ = ::socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
     if (fd_ < 0) throw IoError("relay client: socket() failed");
     if (::connect(fd_, reinterpret_cast<const sockaddr*>(&a), sizeof a) == 0) break;
