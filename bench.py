@@ -311,21 +311,14 @@ def main_ours(args, rank, world, local_rank):
         log(f"[bench] rank {rank}: concurrent host-link ceiling: DMA {link['dma_gbps']} GB/s, "
             f"SM stores {link['sm_store_gbps']} GB/s, NUMA node {link['numa_node']}")
 
-        # uplink relay: ranks whose concurrent link is much slower hand a share
-        # of their large tensors to a rank with spare link (relay.hpp)
-        relay = relay_plan([l["dma_gbps"] for l in links], args.relay)
+        # uplink relay (relay.hpp): every rank can serve; the pairs are chosen
+        # below from the ranks' measured snapshot rates
+        use_relay = world > 1 and args.relay != "off"
         sock = lambda r: f"/tmp/lzk_relay_{os.environ.get('MASTER_PORT', 'solo')}_{r}.sock"  # noqa: E731
-        helper_of = {o: (h, sh) for o, h, sh in relay["pairs"]}
-        serves = any(h == rank for _, h, _ in relay["pairs"])
         pool_bytes = int(built.bytes * 1.01) + (256 << 20)
         cfg = lz.EngineConfig(checkpoint_root=os.path.join(tmp, "ckpt"), host_buffer_bytes=pool_bytes,
                               large_leaf_threshold=1 << 20, fsync_on_finalize=False, flush_discard=True,
-                              hugepages=True, device=dev,
-                              relay_serve_socket=sock(rank) if serves else "",
-                              relay_peer_socket=sock(helper_of[rank][0]) if rank in helper_of else "",
-                              relay_share=helper_of[rank][1] if rank in helper_of else 0.0)
-        if relay["pairs"]:
-            log(f"[bench] rank {rank}: uplink relay {relay}")
+                              hugepages=True, device=dev, relay_serve_socket=sock(rank) if use_relay else "")
         t0 = time.time()
         eng = lz.Engine(cfg, built.topo, built.rank)
         log(f"[bench] rank {rank}: pinned {pool_bytes / 1e9:.1f} GB pool in {time.time() - t0:.1f} s")
@@ -370,6 +363,21 @@ def main_ours(args, rank, world, local_rank):
         # (tools/interference.py) even on boxes where it edges out the DMA
         # engines. All three variants are reported in variants_gbps.
         eng.set_copy_variant(ce_threshold=2 << 20)
+        # uplink relay: ranks whose measured snapshot rate (hybrid, all ranks at
+        # once) is well below the fastest hand a share of their large tensors
+        # to a fast rank; the probes alone mispredict some boxes
+        rank_rates = gather(variants["hybrid"])
+        relay = relay_plan(rank_rates, args.relay if use_relay else "off")
+        helper_of = {o: (h, sh) for o, h, sh in relay["pairs"]}
+
+        def arm_relay(e):
+            if rank in helper_of:
+                e.set_relay(sock(helper_of[rank][0]), helper_of[rank][1])
+            barrier()
+
+        if relay["pairs"]:
+            log(f"[bench] rank {rank}: uplink relay {relay}")
+            arm_relay(eng)
 
         # ---- timed region ----
         for s in range(args.warmup):
@@ -410,6 +418,8 @@ def main_ours(args, rank, world, local_rank):
             except Exception as e:  # optional phase: keep the headline number
                 streaming = {"error": f"{type(e).__name__}: {e}"}
             eng = lz.Engine(cfg, built.topo, built.rank)
+            if relay["pairs"]:
+                arm_relay(eng)
 
         # ---- per-iteration stall under synthetic fwd/bwd, host-memory tier ----
         stall, gemm = None, None
@@ -555,8 +565,8 @@ class PcieSampler:
 
 
 def relay_plan(rates, mode):
-    """Uplink relay pairs from the ranks' concurrently probed copy-engine
-    rates: each rank well below the fastest (< 80 %) hands `share` of every
+    """Uplink relay pairs from the ranks' snapshot rates measured all at once:
+    each rank well below the fastest (< 80 %) hands `share` of every
     shard file's payload to one of the fastest ranks, chosen so that both
     finish together, (1 - x) / r_owner = (1 + x) / r_helper, damped by 10 %
     and capped at 0.45. mode: auto | off | force (pair ranks 2k -> 2k+1 at

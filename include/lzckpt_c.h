@@ -254,6 +254,9 @@ int lzckpt_engine_numa_node(const lzckpt_engine* e);
  * bytes and requests it relayed for owners (helper). */
 int lzckpt_engine_relay_stats(const lzckpt_engine* e, uint64_t* delegated_bytes, uint64_t* served_bytes,
                               uint64_t* served_requests);
+/* Engine::set_relay: delegate `share` of each shard file's payload to the
+ * helper serving `peer_socket` (share 0: off); call between captures. */
+int lzckpt_engine_set_relay(lzckpt_engine* e, const char* peer_socket, double share);
 /* Phase one of the 2PC for THIS rank only (EngineCommitParticipant::prepare,
  * reference consolidation.cpp:142-152): waits until the capture is persisted,
  * then validates the rank's files on the GPU. Writes a JSON vote

@@ -162,6 +162,7 @@ ENGINE_SYMBOLS = [
     ("lzckpt_numa_page_nodes", i32, [vp, u64, u64, P(i32), u64, P(u64)]),
     ("lzckpt_engine_numa_node", i32, [vp]),
     ("lzckpt_engine_relay_stats", i32, [vp, P(u64), P(u64), P(u64)]),
+    ("lzckpt_engine_set_relay", i32, [vp, cp, f64]),
     ("lzckpt_engine_prepare", i32, [vp, P(ModelSpecC), vp, cp, u64, P(u64)]),
     ("lzckpt_engine_ticket_header", i32, [vp, vp, u32, P(vp)]),
     ("lzckpt_engine_restore_file", i32, [vp, cp, vp, P(vp)]),

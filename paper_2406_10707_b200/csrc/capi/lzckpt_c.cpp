@@ -636,6 +636,13 @@ int lzckpt_numa_page_nodes(const void* p, uint64_t len, uint64_t stride, int* no
 
 int lzckpt_engine_numa_node(const lzckpt_engine* e) { return e ? e->e->pool().numa_node() : -1; }
 
+int lzckpt_engine_set_relay(lzckpt_engine* e, const char* peer_socket, double share) {
+  return guard([&] {
+    need(e, "engine");
+    e->e->set_relay(peer_socket ? peer_socket : "", share);
+  });
+}
+
 int lzckpt_engine_relay_stats(const lzckpt_engine* e, uint64_t* delegated_bytes, uint64_t* served_bytes,
                               uint64_t* served_requests) {
   return guard([&] {

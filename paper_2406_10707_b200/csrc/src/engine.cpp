@@ -158,10 +158,7 @@ Engine::Engine(EngineConfig config, ParallelTopology topo, RankCoord rank)
     relay_server_ = std::make_unique<detail::RelayServer>(transfers_.device(), config_.relay.serve_socket,
                                                           config_.relay.staging_bytes, config_.relay.ctas);
   }
-  if (!config_.relay.peer_socket.empty() && config_.relay.share > 0) {
-    if (config_.relay.share >= 1) throw ConfigError("relay share must be below 1");
-    relay_client_ = std::make_unique<detail::RelayClient>(config_.relay.peer_socket);
-  }
+  if (!config_.relay.peer_socket.empty() && config_.relay.share > 0) set_relay(config_.relay.peer_socket, config_.relay.share);
 }
 
 Engine::~Engine() {
@@ -500,14 +497,19 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
     counters_.last_capture_seconds = dt;
     return ticket;
   }
-  const bool relay = relay_client_ && config_.copy_channel.bandwidth_Bps <= 0;
+  double share = 0;
+  {
+    std::lock_guard lk(relay_mu_);
+    share = relay_client_ ? relay_share_ : 0;
+  }
+  const bool relay = share > 0 && config_.copy_channel.bandwidth_Bps <= 0;
   for (auto& b : builds) {
     // Uplink relay: a suffix of the file's large region leaves, up to `share`
     // of its payload, goes to the helper (its bytes never enter this ring).
     size_t own = b.larges.size();
     if (relay) {
       uint64_t moved = 0;
-      const uint64_t budget = uint64_t(config_.relay.share * double(b.payload));
+      const uint64_t budget = uint64_t(share * double(b.payload));
       while (own > 0) {
         const auto& l = b.larges[own - 1];
         if (!l.region || l.size < config_.relay.min_entry || moved + l.size > budget) break;
@@ -874,6 +876,20 @@ void Engine::relay_submit(const std::shared_ptr<CaptureTicket>& ticket, const st
     flush_.complete_external(file_id, false, {});
     throw;
   }
+}
+
+void Engine::set_relay(const std::string& peer_socket, double share) {
+  if (share < 0 || share >= 1) throw ConfigError("relay share must be in [0, 1)");
+  std::unique_ptr<detail::RelayClient> fresh;
+  bool need = false;
+  {
+    std::lock_guard lk(relay_mu_);
+    need = share > 0 && !relay_client_;
+  }
+  if (need) fresh = std::make_unique<detail::RelayClient>(peer_socket);  // connects (may wait for the helper)
+  std::lock_guard lk(relay_mu_);
+  if (fresh) relay_client_ = std::move(fresh);
+  relay_share_ = share;
 }
 
 Engine::RelayStats Engine::relay_stats() const {

@@ -754,6 +754,11 @@ class Engine:
         """NUMA node of this engine's pinned ring and threads (-1: none)."""
         return lib.lzckpt_engine_numa_node(self._h)
 
+    def set_relay(self, peer_socket: str, share: float) -> None:
+        """Delegate `share` of each shard file's payload to the helper serving
+        `peer_socket` (share 0: off). Call between captures."""
+        _check(lib.lzckpt_engine_set_relay(self._h, os.fspath(peer_socket).encode(), share))
+
     def relay_stats(self) -> dict:
         """Uplink relay counters: bytes delegated to the helper (owner), bytes
         and requests relayed for owners (helper)."""
