@@ -376,8 +376,19 @@ def main_ours(args, rank, world, local_rank):
             barrier()
 
         if relay["pairs"]:
-            log(f"[bench] rank {rank}: uplink relay {relay}")
             arm_relay(eng)
+            # one refinement: re-derive each pair's share from the ranks' times
+            # with the relay on (effective rates r = bytes / time)
+            ts = []
+            for s in range(2):
+                barrier()
+                dms, hms, _, _ = snap(30 + s)
+                ts.append(max(dms, hms) * 1e-3)
+            times = gather(statistics.mean(ts))
+            relay = refine_relay(relay, times)
+            helper_of = {o: (h, sh) for o, h, sh in relay["pairs"]}
+            arm_relay(eng)
+            log(f"[bench] rank {rank}: uplink relay {relay}")
 
         # ---- timed region ----
         for s in range(args.warmup):
@@ -585,6 +596,20 @@ def relay_plan(rates, mode):
         x = 0.9 * (rates[h] - rates[o]) / (rates[h] + rates[o])
         out["pairs"].append((o, h, round(min(0.45, x), 3)))
     return out
+
+
+def refine_relay(relay, times):
+    """Second pass of the relay plan: with the relay on, rank i moved
+    (1 -/+ x) of one shard in times[i]; its effective rate is that over the
+    time, and the share that equalises owner and helper is re-derived
+    (undamped, capped at 0.45)."""
+    pairs = []
+    for o, h, x in relay["pairs"]:
+        r_o = (1 - x) / max(times[o], 1e-9)
+        r_h = (1 + x) / max(times[h], 1e-9)
+        pairs.append((o, h, round(min(0.45, max(0.0, (r_h - r_o) / (r_h + r_o))), 3)))
+    return dict(relay, pairs=pairs, first_pass=relay["pairs"],
+                first_pass_times_s=[round(t, 3) for t in times])
 
 
 def sum_stats(stats, sum_over_ranks):
