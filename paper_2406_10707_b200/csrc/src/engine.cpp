@@ -805,16 +805,13 @@ void Engine::relay_submit(const std::shared_ptr<CaptureTicket>& ticket, const st
   {
     std::lock_guard lk(relay_mu_);
     for (size_t i = 0; i < regions.size(); ++i) {
-      const void* ptr = regions[i]->device_ptr();
-      auto it = relay_exports_.find(ptr);
-      if (it == relay_exports_.end()) {
-        lzk_ipc_handle h;
-        uint64_t off = 0;
-        ck(lzk_ipc_export_mem(regions[i]->device(), ptr, &h, &off), "relay: export a leaf");
-        it = relay_exports_.emplace(ptr, std::make_pair(h, off)).first;
-      }
-      entries[i].mem = it->second.first;
-      entries[i].src_offset = it->second.second;
+      // exported at every capture: an allocation freed and re-made at the
+      // same address gets a new handle, which a cache keyed by address
+      // would miss (the helper would then read the old allocation)
+      uint64_t off = 0;
+      ck(lzk_ipc_export_mem(regions[i]->device(), regions[i]->device_ptr(), &entries[i].mem, &off),
+         "relay: export a leaf");
+      entries[i].src_offset = off;
       entries[i].length = sizes[i];
       entries[i].file_offset = file_offsets[i];
       versions[i] = regions[i]->version();

@@ -254,6 +254,20 @@ void RelayServer::handle(int fd, Request& r) {
   int file = -1;
   try {
     const size_t n = r.entries.size();
+    // Mappings of the owners' allocations are kept between requests; an
+    // owner that frees and re-allocates tensors produces new handles, and the
+    // old mappings would pin its freed memory. Drop them all past a bound
+    // (no request is in flight here: requests are handled one at a time).
+    for (const auto& e : r.entries) {
+      opened_.insert(std::string(reinterpret_cast<const char*>(&e.mem), sizeof e.mem));
+    }
+    if (opened_.size() > kMaxOpen) {
+      lzk_ipc_close_all();
+      opened_.clear();
+      for (const auto& e : r.entries) {
+        opened_.insert(std::string(reinterpret_cast<const char*>(&e.mem), sizeof e.mem));
+      }
+    }
     std::vector<const std::byte*> src(n);
     for (size_t i = 0; i < n; ++i) {
       void* base = nullptr;

@@ -33,6 +33,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <set>
 #include <string>
 #include <thread>
 #include <vector>
@@ -85,6 +86,8 @@ class RelayServer {
   uint64_t* digests_ = nullptr;      // pinned, mapped: per-entry FNV results
   uint32_t digest_cap_ = 0;
   std::map<std::string, lzk_event*> events_;  // opened producer events by handle bytes
+  static constexpr size_t kMaxOpen = 4096;    // owners' allocations kept mapped
+  std::set<std::string> opened_;
 
   mutable std::mutex mu_;  // one request at a time (the staging is shared)
   uint64_t bytes_ = 0;
