@@ -576,10 +576,11 @@ class PcieSampler:
 
 
 def relay_plan(rates, mode):
-    """Uplink relay pairs from the ranks' snapshot rates measured all at once:
-    each rank well below the fastest (< 80 %) hands `share` of every
-    shard file's payload to one of the fastest ranks, chosen so that both
-    finish together, (1 - x) / r_owner = (1 + x) / r_helper, damped by 10 %
+    """Uplink relay pairs from the ranks' snapshot rates measured all at once.
+    Ranks well below the fastest (< 80 %) are owners; ranks at >= 90 % of it
+    are helpers; owners are dealt to helpers round-robin (slowest first). A
+    helper h with k owners of mean rate r_o takes share x of each, chosen so
+    that all finish together: (1 - x) / r_o = (1 + k x) / r_h, damped by 10 %
     and capped at 0.45. mode: auto | off | force (pair ranks 2k -> 2k+1 at
     0.3 whatever the rates: exercises the path on symmetric boxes)."""
     n = len(rates)
@@ -592,22 +593,34 @@ def relay_plan(rates, mode):
     top = max(rates)
     owners = sorted((r for r in range(n) if rates[r] < 0.8 * top), key=lambda r: rates[r])
     helpers = sorted((r for r in range(n) if rates[r] >= 0.9 * top), key=lambda r: -rates[r])
-    for o, h in zip(owners, helpers):
-        x = 0.9 * (rates[h] - rates[o]) / (rates[h] + rates[o])
-        out["pairs"].append((o, h, round(min(0.45, x), 3)))
+    if not owners or not helpers:
+        return out
+    groups = {h: [] for h in helpers}
+    for i, o in enumerate(owners):
+        groups[helpers[i % len(helpers)]].append(o)
+    for h, os_ in groups.items():
+        if not os_:
+            continue
+        r_o = sum(rates[o] for o in os_) / len(os_)
+        x = 0.9 * (rates[h] - r_o) / (rates[h] + len(os_) * r_o)
+        out["pairs"] += [(o, h, round(min(0.45, max(0.0, x)), 3)) for o in os_]
     return out
 
 
 def refine_relay(relay, times):
-    """Second pass of the relay plan: with the relay on, rank i moved
-    (1 -/+ x) of one shard in times[i]; its effective rate is that over the
-    time, and the share that equalises owner and helper is re-derived
-    (undamped, capped at 0.45)."""
-    pairs = []
+    """Second pass of the relay plan. With the relay on, owner o moved
+    (1 - x_o) of a shard in times[o] and helper h moved 1 + sum(x) in
+    times[h]; those effective rates give each helper group's equalising share
+    again (undamped, capped at 0.45)."""
+    groups = {}
     for o, h, x in relay["pairs"]:
-        r_o = (1 - x) / max(times[o], 1e-9)
-        r_h = (1 + x) / max(times[h], 1e-9)
-        pairs.append((o, h, round(min(0.45, max(0.0, (r_h - r_o) / (r_h + r_o))), 3)))
+        groups.setdefault(h, []).append((o, x))
+    pairs = []
+    for h, os_ in groups.items():
+        r_h = (1 + sum(x for _, x in os_)) / max(times[h], 1e-9)
+        r_o = sum((1 - x) / max(times[o], 1e-9) for o, x in os_) / len(os_)
+        x = (r_h - r_o) / (r_h + len(os_) * r_o)
+        pairs += [(o, h, round(min(0.45, max(0.0, x)), 3)) for o, _ in os_]
     return dict(relay, pairs=pairs, first_pass=relay["pairs"],
                 first_pass_times_s=[round(t, 3) for t in times])
 
