@@ -22,6 +22,11 @@ reference arm's exact sample), e2e (capture -> files durable through the
 public API), the CPU reference engine timed on this box's cores, clocks
 during the timed region, and the number of our kernel launches.
 
+At N>1 every rank also serves the uplink relay (relay.hpp): after the variant
+sweep, ranks whose measured snapshot rate is well below the fastest hand a
+share of their large tensors to the fastest ranks, which read them over
+NVLink and push them through their own host link (--relay auto|off|force).
+
 --impl reference runs the unmodified reference engine (oracle/_ref) on the
 same config with none of this repo's libraries loaded.
 """
