@@ -382,17 +382,23 @@ def main_ours(args, rank, world, local_rank):
 
         if relay["pairs"]:
             arm_relay(eng)
-            # one refinement: re-derive each pair's share from the ranks' times
-            # with the relay on (effective rates r = bytes / time)
-            ts = []
-            for s in range(2):
-                barrier()
-                dms, hms, _, _ = snap(30 + s)
-                ts.append(max(dms, hms) * 1e-3)
-            times = gather(statistics.mean(ts))
-            relay = refine_relay(relay, times)
-            helper_of = {o: (h, sh) for o, h, sh in relay["pairs"]}
-            arm_relay(eng)
+            # two refinements: re-derive each group's shares from the ranks'
+            # times with the relay on (effective rates r = bytes / time)
+            history = []
+            for it in range(2):
+                ts = []
+                for s in range(2):
+                    barrier()
+                    dms, hms, _, _ = snap(30 + 2 * it + s)
+                    ts.append(max(dms, hms) * 1e-3)
+                times = gather(statistics.mean(ts))
+                history.append({"pairs": relay["pairs"], "times_s": [round(t, 3) for t in times]})
+                relay = refine_relay(relay, times)
+                helper_of = {o: (h, sh) for o, h, sh in relay["pairs"]}
+                arm_relay(eng)
+            relay["history"] = history
+            relay.pop("first_pass", None)
+            relay.pop("first_pass_times_s", None)
             log(f"[bench] rank {rank}: uplink relay {relay}")
 
         # ---- timed region ----
@@ -445,6 +451,8 @@ def main_ours(args, rank, world, local_rank):
                 stall = train_stall(lz, torch, eng, plan, built.tree, gemm, barrier, step0=500)
             except Exception as e:
                 stall = {"error": f"{type(e).__name__}: {e}"}
+            if world > 1:  # every rank ran its own loop (owners and helpers alike)
+                stall["per_rank"] = gather({k: stall.get(k) for k in ("iter_overhead", "stall_def_ms", "stall_ms")})
         barrier()
         eng.close()
         del eng
