@@ -799,60 +799,23 @@ void Engine::relay_submit(const std::shared_ptr<CaptureTicket>& ticket, const st
                           uint64_t file_id, const std::vector<std::shared_ptr<DeviceRegion>>& regions,
                           const std::vector<uint64_t>& sizes, const std::vector<uint64_t>& file_offsets,
                           void* producer_stream, bool ordered) {
-  std::vector<detail::RelayEntry> entries(regions.size());
-  std::vector<uint64_t> versions(regions.size());
-  uint64_t bytes = 0;
-  {
-    std::lock_guard lk(relay_mu_);
-    for (size_t i = 0; i < regions.size(); ++i) {
-      // exported at every capture: an allocation freed and re-made at the
-      // same address gets a new handle, which a cache keyed by address
-      // would miss (the helper would then read the old allocation)
-      uint64_t off = 0;
-      ck(lzk_ipc_export_mem(regions[i]->device(), regions[i]->device_ptr(), &entries[i].mem, &off),
-         "relay: export a leaf");
-      entries[i].src_offset = off;
-      entries[i].length = sizes[i];
-      entries[i].file_offset = file_offsets[i];
-      versions[i] = regions[i]->version();
-      bytes += sizes[i];
-    }
-    relay_delegated_ += bytes;
-  }
-  // producer ordering across processes: an interprocess event on the trainer's stream
-  lzk_event* ev = nullptr;
-  lzk_ipc_handle evh{};
-  if (ordered) {
-    {
-      std::lock_guard lk(relay_mu_);
-      if (!relay_events_.empty()) {
-        std::tie(ev, evh) = relay_events_.back();
-        relay_events_.pop_back();
-      }
-    }
-    if (!ev) ck(lzk_ipc_event_create(transfers_.device(), &ev, &evh), "relay: producer event");
-    ck(lzk_event_record_raw(ev, producer_stream), "relay: record on the producer stream");
-  }
-  uint32_t flags = 0;
-  if (!config_.flush.discard) flags |= detail::kRelayHash;
-  if (!config_.flush.discard && !config_.flush.hash_only) flags |= detail::kRelayWrite;
-  if (!config_.flush.discard && config_.flush.fsync_on_finalize) flags |= detail::kRelayFsync;
   {
     std::lock_guard tl(ticket->mu_);
     ++ticket->relay_reads_pending_;
   }
+  std::vector<uint64_t> versions(regions.size());
+  for (size_t i = 0; i < regions.size(); ++i) versions[i] = regions[i]->version();
   std::weak_ptr<CaptureTicket> weak = ticket;
   const uint64_t ticket_id = ticket->id_;
-  auto on_read = [this, weak, ticket_id, regions, versions, ev, evh](bool ok, const std::string& err) {
-    if (ev) {
-      std::lock_guard lk(relay_mu_);
-      relay_events_.emplace_back(ev, evh);  // the helper has consumed its wait
-    }
+  lzk_event* ev = nullptr;
+  lzk_ipc_handle evh{};
+  // READ_DONE (or a failure): settle the ticket's relay part
+  auto on_read = [this, weak, ticket_id, regions, versions](bool ok, const std::string& err) {
     bool torn = false;
     for (size_t i = 0; i < regions.size(); ++i) torn = torn || regions[i]->version() != versions[i];
     auto t = weak.lock();
     if (!t) return;
-    if (torn) on_torn(ticket_id);
+    if (torn && ok) on_torn(ticket_id);
     {
       std::lock_guard tl(t->mu_);
       --t->relay_reads_pending_;
@@ -863,15 +826,60 @@ void Engine::relay_submit(const std::shared_ptr<CaptureTicket>& ticket, const st
     }
     t->done_cv_.notify_all();
   };
-  auto on_persisted = [this, file_id](bool ok, const std::string&, const std::vector<uint64_t>& sums) {
-    flush_.complete_external(file_id, ok, sums);
-  };
   try {
-    relay_client_->submit(path, flags, ev ? &evh : nullptr, entries, on_read, on_persisted);
-  } catch (...) {
-    on_read(false, "uplink relay: request not delivered");
+    std::vector<detail::RelayEntry> entries(regions.size());
+    uint64_t bytes = 0;
+    for (size_t i = 0; i < regions.size(); ++i) {
+      // exported at every capture: an allocation freed and re-made at the
+      // same address gets a new handle, which a cache keyed by address
+      // would miss (the helper would then read the old allocation)
+      uint64_t off = 0;
+      ck(lzk_ipc_export_mem(regions[i]->device(), regions[i]->device_ptr(), &entries[i].mem, &off),
+         "relay: export a leaf");
+      entries[i].src_offset = off;
+      entries[i].length = sizes[i];
+      entries[i].file_offset = file_offsets[i];
+      bytes += sizes[i];
+    }
+    // producer ordering across processes: an interprocess event on the trainer's stream
+    if (ordered) {
+      {
+        std::lock_guard lk(relay_mu_);
+        if (!relay_events_.empty()) {
+          std::tie(ev, evh) = relay_events_.back();
+          relay_events_.pop_back();
+        }
+      }
+      if (!ev) ck(lzk_ipc_event_create(transfers_.device(), &ev, &evh), "relay: producer event");
+      ck(lzk_event_record_raw(ev, producer_stream), "relay: record on the producer stream");
+    }
+    uint32_t flags = 0;
+    if (!config_.flush.discard) flags |= detail::kRelayHash;
+    if (!config_.flush.discard && !config_.flush.hash_only) flags |= detail::kRelayWrite;
+    if (!config_.flush.discard && config_.flush.fsync_on_finalize) flags |= detail::kRelayFsync;
+    lzk_event* used = ev;
+    auto read_done = [this, on_read, used, evh](bool ok, const std::string& err) {
+      if (used) {
+        std::lock_guard lk(relay_mu_);
+        relay_events_.emplace_back(used, evh);  // the helper has consumed its wait
+      }
+      on_read(ok, err);
+    };
+    auto persisted = [this, file_id](bool ok, const std::string&, const std::vector<uint64_t>& sums) {
+      flush_.complete_external(file_id, ok, sums);
+    };
+    relay_client_->submit(path, flags, ev ? &evh : nullptr, entries, read_done, persisted);
+    std::lock_guard lk(relay_mu_);
+    relay_delegated_ += bytes;
+  } catch (const std::exception& e) {
+    // The helper is unreachable: the ticket fails (its own copies still run,
+    // so the pool drains) and the file ends without a header.
+    if (ev) {
+      std::lock_guard lk(relay_mu_);
+      relay_events_.emplace_back(ev, evh);
+    }
+    on_read(false, e.what());
     flush_.complete_external(file_id, false, {});
-    throw;
   }
 }
 

@@ -138,3 +138,73 @@ def test_relay_discard_tier_completes(lz, tmp_path, helper):
         assert not t.torn()
     assert eng.relay_stats()["delegated_bytes"] > 0
     eng.close()
+
+
+def test_relay_tear_is_detected(lz, tmp_path, helper):
+    """A delegated leaf mutated (declared) before the helper has read it tears
+    the ticket, as a local copy would (reference transfer_engine.cpp:146-154):
+    the helper's read waits behind a 100 ms kernel on the producer stream."""
+    torch = pytest.importorskip("torch")
+    w, thr = workload()
+    tree = lz.StateTree()
+    regions, keep = {}, []
+    for _, path, size in w.leaves:
+        t = torch.zeros(size, dtype=torch.uint8, device="cuda:0")
+        keep.append(t)
+        regions[path] = lz.DeviceRegion.wrap(t)
+        tree.set_region(path, regions[path])
+    torch.cuda.synchronize()
+    eng = lz.Engine(lz.EngineConfig(checkpoint_root=str(tmp_path / "t"), host_buffer_bytes=256 << 20, device=0,
+                                    large_leaf_threshold=thr, fsync_on_finalize=False,
+                                    relay_peer_socket=helper, relay_share=0.6, relay_min_entry=1 << 20),
+                    lz.ParallelTopology(1, 1, 1, 1, 1), lz.RankCoord())
+    plan = lz.plan_checkpoint(lz.ParallelTopology(1, 1, 1, 1, 1),
+                              lz.ModelSpec(param_count=w.param_count, layer_count=w.layer_count), 1)
+    torch.cuda._sleep(200_000_000)  # the helper's read waits behind this
+    t = eng.capture(plan, tree, 1)
+    regions["optim/v3"].bump_version()  # a delegated leaf changes before it was read
+    with pytest.raises(lz.TornSnapshot):
+        eng.update_barrier(t)
+    assert t.torn()
+    eng.drain()
+    for f in t.shard_files():  # no header was written: the files are incomplete
+        with pytest.raises(lz.Error):
+            lz.read_header(f)
+    eng.close()
+
+
+def test_lost_helper_fails_loudly(lz, tmp_path):
+    """The helper process dies: the owner's next capture raises instead of
+    hanging, and closing the engine returns."""
+    torch = pytest.importorskip("torch")
+    if torch.cuda.device_count() < 2:
+        pytest.skip("the relay needs two GPUs (run with gpurun --gpus 2)")
+    sock = str(tmp_path / "relay.sock")
+    env = dict(os.environ, LZK_ROOT=ROOT, LZK_TMP=str(tmp_path), LZK_SOCK=sock)
+    p = subprocess.Popen([sys.executable, "-c", HELPER], env=env, stdout=subprocess.DEVNULL,
+                         stderr=subprocess.DEVNULL)
+    t0 = time.time()
+    while not os.path.exists(sock + ".ready"):
+        assert p.poll() is None and time.time() - t0 < 120
+        time.sleep(0.05)
+    w, thr = workload()
+    tree = lz.StateTree()
+    keep = []
+    for _, path, size in w.leaves:
+        t = torch.zeros(size, dtype=torch.uint8, device="cuda:0")
+        keep.append(t)
+        tree.set_region(path, lz.DeviceRegion.wrap(t))
+    eng = lz.Engine(lz.EngineConfig(checkpoint_root=str(tmp_path / "l"), host_buffer_bytes=256 << 20, device=0,
+                                    large_leaf_threshold=thr, fsync_on_finalize=False,
+                                    relay_peer_socket=sock, relay_share=0.6, relay_min_entry=1 << 20),
+                    lz.ParallelTopology(1, 1, 1, 1, 1), lz.RankCoord())
+    p.kill()
+    p.wait(timeout=60)
+    time.sleep(0.5)  # the owner's reader sees the closed connection
+    plan = lz.plan_checkpoint(lz.ParallelTopology(1, 1, 1, 1, 1),
+                              lz.ModelSpec(param_count=w.param_count, layer_count=w.layer_count), 1)
+    with pytest.raises(lz.Error):
+        t = eng.capture(plan, tree, 1)
+        eng.update_barrier(t)
+        eng.wait_persisted(t)
+    eng.close()
