@@ -325,7 +325,16 @@ def main_ours(args, rank, world, local_rank):
                               large_leaf_threshold=1 << 20, fsync_on_finalize=False, flush_discard=True,
                               hugepages=True, device=dev, relay_serve_socket=sock(rank) if use_relay else "")
         t0 = time.time()
-        eng = lz.Engine(cfg, built.topo, built.rank)
+        try:
+            eng = lz.Engine(cfg, built.topo, built.rank)
+        except lz.Error as e:  # e.g. the relay server could not start: run without it
+            if not use_relay:
+                raise
+            log(f"[bench] rank {rank}: engine with relay server failed ({e}); relay off")
+            cfg.relay_serve_socket = ""
+            eng = lz.Engine(cfg, built.topo, built.rank)
+        if use_relay and not all(gather(bool(cfg.relay_serve_socket))):
+            use_relay = False  # every rank must serve for any plan to be valid
         log(f"[bench] rank {rank}: pinned {pool_bytes / 1e9:.1f} GB pool in {time.time() - t0:.1f} s")
         plan = lz.plan_checkpoint(built.topo, built.model, built.step)
         producer = torch.cuda.current_stream(dev)
