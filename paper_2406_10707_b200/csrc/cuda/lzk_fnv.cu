@@ -83,7 +83,6 @@ constexpr uint64_t cpow(uint64_t b, uint64_t e) {
   }
   return r;
 }
-constexpr uint64_t kP8 = cpow(kPrime, 8);
 constexpr uint64_t kP16 = cpow(kPrime, 16);
 constexpr uint64_t kP1024 = cpow(kPrime, 1024);
 
@@ -181,12 +180,12 @@ __device__ __forceinline__ void to_planes(const uint32_t* w, uint32_t* B) {
 // at the lane's offsets 0 and 16 (meaningful when NP == 8). The kernel is
 // bound by the ALU pipe, so bit bookkeeping uses multiplies (FMA pipe) and the
 // carries stay unpacked.
-template <int NP, bool QUARTERS = false>
+template <int NP>
 __device__ __forceinline__ void scan_planes(const uint32_t* w, uint32_t* carry, uint32_t lt, uint32_t valid,
-                                            uint32_t& l0, uint32_t& l16, uint32_t* l8_24 = nullptr) {
+                                            uint32_t& l0, uint32_t& l16) {
   uint32_t B[8];
   to_planes(w, B);
-  uint32_t lstart = 0, q = 0, q8 = 0, q24 = 0;
+  uint32_t lstart = 0, q = 0;
   // plane i: l_i at each position = carry-in xor exclusive prefix-XOR of
   // e_i; returns x_i = l_i ^ b_i. Bit 16 of l_i is bit 15 of the prefix
   // xor the carry-in, so the offset-16 low byte is lstart ^ (q >> 15).
@@ -202,10 +201,6 @@ __device__ __forceinline__ void scan_planes(const uint32_t* w, uint32_t* carry, 
     carry[i] ^= __popc(bal) & 1u;
     lstart += cin * (1u << i);
     q += (p & 0x8000u) * (1u << i);
-    if constexpr (QUARTERS) {
-      q8 += (p & 0x80u) * (1u << i);
-      q24 += ((p >> 16) & 0x80u) * (1u << i);
-    }
     return (p << 1) ^ (cin * 0xffffffffu) ^ B[i];
   };
   // column adder of y = 179 x (mod 256): column i sums x_i, x_{i-1},
@@ -242,10 +237,6 @@ __device__ __forceinline__ void scan_planes(const uint32_t* w, uint32_t* carry, 
   }
   l0 = lstart;
   l16 = lstart ^ (q >> 15);
-  if constexpr (QUARTERS) {
-    l8_24[0] = lstart ^ (q8 >> 7);
-    l8_24[1] = lstart ^ (q24 >> 7);
-  }
 }
 
 __device__ __forceinline__ uint64_t warp_sum(uint64_t v) {
@@ -289,19 +280,14 @@ __device__ uint64_t hash_range(const uint8_t* p, uint64_t n, uint64_t h, uint32_
         b = ld_nc(q + 1);
       }
       uint32_t l0, l16;
-      // four independent 8-byte FNV chains per lane (offsets 0, 8, 16, 24)
-      uint32_t lq[2];
-      scan_planes<8, true>(w, carry, lt, 0xffffffffu, l0, l16, lq);
-      uint64_t a0 = l0, a1 = lq[0], a2 = l16, a3 = lq[1];
+      scan_planes<8>(w, carry, lt, 0xffffffffu, l0, l16);
+      uint64_t a0 = l0, a1 = l16;
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
+      for (int k = 0; k < 4; ++k) {
         a0 = fnv_word(a0, w[k]);
-        a1 = fnv_word(a1, w[k + 2]);
-        a2 = fnv_word(a2, w[k + 4]);
-        a3 = fnv_word(a3, w[k + 6]);
+        a1 = fnv_word(a1, w[k + 4]);
       }
-      R = R * kP1024 + (((a0 - kP8 * l0) * kP8 + (a1 - kP8 * lq[0])) * kP16 +
-                        ((a2 - kP8 * l16) * kP8 + (a3 - kP8 * lq[1])));
+      R = R * kP1024 + ((a0 - kP16 * l0) * kP16 + (a1 - kP16 * l16));
     }
     h = pow64(kP1024, windows) * h + warp_sum(R * wlane);
   }
