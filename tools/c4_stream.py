@@ -19,7 +19,7 @@ tmp = tempfile.mkdtemp(prefix="lzk_c4_", dir=bench.ROOT)
 built = lz.build_workload(w.write_spec(os.path.join(tmp, "c4.spec")), 0)
 link = bench.measure_link_ceiling(lz, 0)
 plan = lz.plan_checkpoint(built.topo, built.model, built.step)
-res = bench.measure_streaming(lz, built, plan, built.bytes, tmp, 0, lambda: None, pool=pool, segment=1 << 30)
+res = bench.measure_streaming(lz, built, plan, built.bytes, tmp, 0, lambda: None, None, pool=pool, segment=1 << 30)
 print(json.dumps({"config": "c4-llama70b rank 0 of dp=8 (configs[3])", "payload_bytes": built.bytes,
                   "tensors": len(w.leaves), "pool_bytes": pool, "segment_bytes": 1 << 30, "gbps": res["gbps"],
                   "frac_of_64": round(res["gbps"] / 64.0, 4), "link_dma_gbps": link["dma_gbps"],
