@@ -1,0 +1,62 @@
+"""CPU checks of bench.py's host-side logic: the reference arm must not load
+this repo's package (its process mapped our libraries), both arms
+derive one `config`, and the uplink-relay planner pairs ranks sensibly on the
+box classes seen on the GPU pool (profiles/r02_bench_n4_*)."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+
+
+def test_reference_arm_helpers_do_not_import_the_package():
+    code = ("import sys; sys.path.insert(0, %r); import bench; bench.bench_config(1, 32); "
+            "bench.load_workloads().llama_layer_sample(layers=2); "
+            "print([m for m in sys.modules if m.startswith('paper_2406_10707_b200')])" % ROOT)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, check=True).stdout
+    assert out.strip() == "[]"
+
+
+def test_both_arms_share_one_config():
+    a = bench.bench_config(4, bench.headline_layers(32, 4))
+    b = bench.bench_config(4, bench.headline_layers(32, 4))
+    assert json.dumps(a, sort_keys=True) == json.dumps(b, sort_keys=True)
+    assert a["tensors"] == 36 * bench.headline_layers(32, 4) + 3 * 4  # 9 tensors x 4 states per layer + 3 others
+    assert 1 <= bench.sample_layers(20, 5) <= 4
+
+
+def test_relay_plan_shared_uplink_pair():
+    # ranks 0-1 share an uplink (r02_bench_n4_shared_uplink_relay.json)
+    plan = bench.relay_plan([27.1, 27.1, 44.5, 44.7], "auto")
+    owners = {o for o, _, _ in plan["pairs"]}
+    helpers = {h for _, h, _ in plan["pairs"]}
+    assert owners == {0, 1} and helpers == {2, 3}
+    for o, h, x in plan["pairs"]:
+        assert 0.15 < x < 0.3
+        # equal finishing times under the model, before damping
+        assert abs((1 - x / 0.9) / 27.1 - (1 + x / 0.9) / 44.6) < 0.002
+
+
+def test_relay_plan_three_owners_one_helper():
+    plan = bench.relay_plan([21.9, 21.9, 21.9, 46.2], "auto")
+    assert sorted(o for o, _, _ in plan["pairs"]) == [0, 1, 2]
+    assert {h for _, h, _ in plan["pairs"]} == {3}
+
+
+def test_relay_plan_symmetric_and_off():
+    assert bench.relay_plan([18.4] * 4, "auto")["pairs"] == []
+    assert bench.relay_plan([27.0, 44.0], "off")["pairs"] == []
+    assert bench.relay_plan([57.0] * 4, "force")["pairs"] == [(0, 1, 0.3), (2, 3, 0.3)]
+
+
+def test_refine_moves_toward_equal_times():
+    plan = {"mode": "auto", "rates_gbps": [46, 46, 46, 33.9], "pairs": [(3, 0, 0.14)]}
+    # the owner (rank 3) still finishes last: its share must grow
+    refined = bench.refine_relay(plan, [2.2, 2.0, 2.0, 2.55])
+    assert refined["pairs"][0][2] > 0.14
+    # the helper finishes last: the share must shrink
+    refined = bench.refine_relay(plan, [2.8, 2.0, 2.0, 2.3])
+    assert refined["pairs"][0][2] < 0.14
