@@ -137,6 +137,7 @@ RelayServer::RelayServer(int device, std::string socket_path, uint64_t staging_b
       ctas_(ctas ? ctas : 4) {
   check(lzk_set_device(device_), "relay server: device");
   check(lzk_stream_create(device_, 0, &stream_), "relay server: stream");
+  check(lzk_stream_create(device_, 0, &hash_stream_), "relay server: hash stream");
   const size_t slots = size_t(std::max<uint64_t>(2, staging_bytes / chunk_));
   for (size_t k = 0; k < slots; ++k) {
     void* p = nullptr;
@@ -172,10 +173,12 @@ RelayServer::~RelayServer() {
   for (int fd : conn_fds_) ::close(fd);
   ::unlink(path_.c_str());
   lzk_stream_sync(stream_);
+  lzk_stream_sync(hash_stream_);
   for (auto* e : chunk_done_) lzk_event_destroy(e);
   for (auto& [k, e] : events_) lzk_event_destroy(e);
   for (auto* p : staging_) lzk_host_free(p);
   if (digests_) lzk_host_free(digests_);
+  lzk_stream_destroy(hash_stream_);
   lzk_stream_destroy(stream_);
 }
 
@@ -283,6 +286,7 @@ void RelayServer::handle(int fd, Request& r) {
         it = events_.emplace(key, e).first;
       }
       check(lzk_stream_wait_event(stream_, it->second), "relay: producer wait");
+      if (r.flags & kRelayHash) check(lzk_stream_wait_event(hash_stream_, it->second), "relay: producer wait");
     }
     std::vector<uint64_t> sums;
     if (r.flags & kRelayHash) {
@@ -298,7 +302,8 @@ void RelayServer::handle(int fd, Request& r) {
         hd[i] = {reinterpret_cast<uint64_t>(src[i]), r.entries[i].length, LZK_FNV_BASIS,
                  reinterpret_cast<uint64_t>(digests_ + i)};
       }
-      check(lzk_fnv1a64_batch(stream_, hd.data(), uint32_t(n), 16), "relay: entry checksums");
+      // on its own stream, concurrently with the gathers below
+      check(lzk_fnv1a64_batch(hash_stream_, hd.data(), uint32_t(n), 16), "relay: entry checksums");
     }
     if (r.flags & kRelayWrite) {
       file = ::open(r.path.c_str(), O_WRONLY | O_CLOEXEC);
@@ -350,6 +355,7 @@ void RelayServer::handle(int fd, Request& r) {
       slot = (slot + 1) % slots;
     }
     check(lzk_stream_sync(stream_), "relay: reads");  // every read of the owner's memory is done
+    check(lzk_stream_sync(hash_stream_), "relay: checksums");
     if (r.flags & kRelayHash) sums.assign(digests_, digests_ + n);
     reply(kReadDone, true, "", {});
     read_sent = true;
@@ -366,6 +372,7 @@ void RelayServer::handle(int fd, Request& r) {
   } catch (const std::exception& e) {
     if (file >= 0) ::close(file);
     lzk_stream_sync(stream_);
+    lzk_stream_sync(hash_stream_);
     if (!read_sent) reply(kReadDone, false, e.what(), {});
     reply(kPersisted, false, e.what(), {});
   }

@@ -80,7 +80,8 @@ class RelayServer {
   const uint64_t chunk_;
   const uint32_t ctas_;
   int listen_fd_ = -1;
-  lzk_stream* stream_ = nullptr;
+  lzk_stream* stream_ = nullptr;       // gathers
+  lzk_stream* hash_stream_ = nullptr;  // entry checksums, beside the gathers
   std::vector<std::byte*> staging_;  // pinned, mapped chunks
   std::vector<lzk_event*> chunk_done_;
   uint64_t* digests_ = nullptr;      // pinned, mapped: per-entry FNV results
