@@ -394,7 +394,7 @@ def main_ours(args, rank, world, local_rank):
             # two refinements: re-derive each group's shares from the ranks'
             # times with the relay on (effective rates r = bytes / time)
             history = []
-            for it in range(2):
+            for it in range(2 if relay["mode"] == "auto" else 0):
                 ts = []
                 for s in range(2):
                     barrier()
@@ -405,7 +405,8 @@ def main_ours(args, rank, world, local_rank):
                 relay = refine_relay(relay, times)
                 helper_of = {o: (h, sh) for o, h, sh in relay["pairs"]}
                 arm_relay(eng)
-            relay["history"] = history
+            if history:
+                relay["history"] = history
             relay.pop("first_pass", None)
             relay.pop("first_pass_times_s", None)
             log(f"[bench] rank {rank}: uplink relay {relay}")
