@@ -486,10 +486,10 @@ def main_ours(args, rank, world, local_rank):
 
         # ---- BASELINE configs[2]: the 13B dp=8 plan, rank r -> GPU r ----
         configs2 = None
-        if world > 1 and not args.skip_configs2:
+        if 1 < world <= 8 and not args.skip_configs2:
             try:
                 configs2 = run_configs2(lz, torch, W, dev, tmp, rank, world, barrier, max_over_ranks,
-                                        sum_over_ranks, producer)
+                                        sum_over_ranks, gather, producer, args.relay if use_relay else "off")
             except Exception as e:
                 configs2 = {"error": f"{type(e).__name__}: {e}"}
 
@@ -1018,33 +1018,52 @@ def durable_stall(lz, torch, sbuilt, tmp, dev, gemm, barrier):
             "note": "C2 (108 GB) exceeds the box's 80 GB disk; the shard is the matched sample, the GEMM loop C2's"}
 
 
-def run_configs2(lz, torch, W, dev, tmp, rank, world, barrier, max_over_ranks, sum_over_ranks, producer, steps=3):
+def run_configs2(lz, torch, W, dev, tmp, rank, world, barrier, max_over_ranks, sum_over_ranks, gather, producer,
+                 relay_mode="auto", steps=3):
     """BASELINE configs[2]: LLaMA-13B over dp=8, ~26 GB per GPU, all ranks
     snapshotting at once. Rank r owns plan rank r of the dp=8 plan; at N=8 this
-    is the whole configuration, at N<8 its first N ranks."""
-    if rank >= 8:
-        return None
+    is the whole configuration, at N<8 its first N ranks. The uplink relay is
+    planned from this block's own measured per-rank rates, as for the
+    headline."""
     w = W.llama13b_shard(dp=8, rank=rank)
     built = lz.build_workload(w.write_spec(os.path.join(tmp, "c3.spec")), dev)
+    use_relay = relay_mode != "off"
+    sock = lambda r: f"/tmp/lzk_relay_c3_{os.environ.get('MASTER_PORT', 'solo')}_{r}.sock"  # noqa: E731
     cfg = lz.EngineConfig(checkpoint_root=os.path.join(tmp, "ckpt_c3"), host_buffer_bytes=int(built.bytes * 1.01) + (256 << 20),
-                          fsync_on_finalize=False, flush_discard=True, device=dev)
+                          fsync_on_finalize=False, flush_discard=True, device=dev,
+                          relay_serve_socket=sock(rank) if use_relay else "")
     eng = lz.Engine(cfg, built.topo, built.rank)
     plan = lz.plan_checkpoint(built.topo, built.model, built.step)
+    step_id = [50]
+
+    def step():
+        barrier()
+        h0 = time.perf_counter()
+        t = eng.capture(plan, built.tree, step_id[0], producer_stream=producer)
+        step_id[0] += 1
+        eng.update_barrier(t)
+        ms = max(eng.ticket_device_ms(t), (time.perf_counter() - h0) * 1e3)
+        eng.wait_persisted(t)
+        return ms, t.payload_bytes()
+
+    relay = {"mode": "off", "pairs": []}
     try:
-        for s in range(2):
+        step()
+        warm_ms, payload = step()
+        if use_relay:
+            relay = relay_plan(gather(round(payload / (warm_ms * 1e-3) / 1e9, 3)), relay_mode)
+            helper_of = {o: (h, sh) for o, h, sh in relay["pairs"]}
+            if rank in helper_of:
+                eng.set_relay(sock(helper_of[rank][0]), helper_of[rank][1])
+            if relay["pairs"] and relay_mode == "auto":
+                times = gather(statistics.mean(step()[0] for _ in range(2)) * 1e-3)
+                relay = refine_relay(relay, times)
+                helper_of = {o: (h, sh) for o, h, sh in relay["pairs"]}
+                if rank in helper_of:
+                    eng.set_relay(sock(helper_of[rank][0]), helper_of[rank][1])
             barrier()
-            t = eng.capture(plan, built.tree, 50 + s, producer_stream=producer)
-            eng.update_barrier(t)
-            eng.wait_persisted(t)
-        ms = []
-        for s in range(steps):
-            barrier()
-            h0 = time.perf_counter()
-            t = eng.capture(plan, built.tree, 60 + s, producer_stream=producer)
-            eng.update_barrier(t)
-            ms.append(max(eng.ticket_device_ms(t), (time.perf_counter() - h0) * 1e3))
-            eng.wait_persisted(t)
-        payload = t.payload_bytes()
+        ms = [step()[0] for _ in range(steps)]
+        barrier()  # a helper must outlive its owners' requests
     finally:
         eng.close()
     t_max = max_over_ranks(sum(ms) * 1e-3)
@@ -1052,7 +1071,8 @@ def run_configs2(lz, torch, W, dev, tmp, rank, world, barrier, max_over_ranks, s
     return {"workload": f"c3-llama13b: plan ranks 0..{min(world, 8) - 1} of the dp=8 13B plan (BASELINE configs[2]"
                         + ("" if world == 8 else f"; {world} of its 8 ranks") + ")",
             "payload_bytes_per_gpu": payload, "value": round(agg / t_max / 1e9, 3), "unit": "GB/s",
-            "per_gpu_gbps": round(payload * steps / (sum(ms) * 1e-3) / 1e9, 3), "steps": steps}
+            "per_gpu_gbps": round(payload * steps / (sum(ms) * 1e-3) / 1e9, 3), "steps": steps,
+            "relay": relay}
 
 
 def main():
