@@ -390,25 +390,26 @@ def main_ours(args, rank, world, local_rank):
             barrier()
 
         if relay["pairs"]:
-            arm_relay(eng)
-            # two refinements: re-derive each group's shares from the ranks'
-            # times with the relay on (effective rates r = bytes / time)
-            history = []
-            for it in range(2 if relay["mode"] == "auto" else 0):
+            tune_step = [30]
+
+            def measure():
                 ts = []
-                for s in range(2):
+                for _ in range(2):
                     barrier()
-                    dms, hms, _, _ = snap(30 + 2 * it + s)
+                    dms, hms, _, _ = snap(tune_step[0])
+                    tune_step[0] += 1
                     ts.append(max(dms, hms) * 1e-3)
-                times = gather(statistics.mean(ts))
-                history.append({"pairs": relay["pairs"], "times_s": [round(t, 3) for t in times]})
-                relay = refine_relay(relay, times)
-                helper_of = {o: (h, sh) for o, h, sh in relay["pairs"]}
-                arm_relay(eng)
-            if history:
-                relay["history"] = history
-            relay.pop("first_pass", None)
-            relay.pop("first_pass_times_s", None)
+                return gather(statistics.mean(ts))
+
+            def arm(p):
+                nonlocal helper_of
+                helper_of = {o: (h, sh) for o, h, sh in p["pairs"]}
+                eng.set_relay(sock(helper_of[rank][0]) if rank in helper_of else "",
+                              helper_of[rank][1] if rank in helper_of else 0.0)
+                barrier()
+
+            base = [payload / (r * 1e9) for r in rank_rates]  # the hybrid sweep, no relay
+            relay = tune_relay(relay, base, measure, arm)
             log(f"[bench] rank {rank}: uplink relay {relay}")
 
         # ---- timed region ----
@@ -630,11 +631,13 @@ def relay_plan(rates, mode):
     return out
 
 
-def refine_relay(relay, times):
-    """Second pass of the relay plan. With the relay on, owner o moved
+def refine_relay(relay, times, damping=1.0):
+    """Next pass of the relay plan. With the relay on, owner o moved
     (1 - x_o) of a shard in times[o] and helper h moved 1 + sum(x) in
-    times[h]; those effective rates give each helper group's equalising share
-    again (undamped, capped at 0.45)."""
+    times[h]; those effective rates give each helper group's equalising
+    share x*, and the share moves `damping` of the way there (capped at
+    0.45). The helper's rate is not constant (its link saturates), hence the
+    damping and tune_relay's keep-the-best rule."""
     groups = {}
     for o, h, x in relay["pairs"]:
         groups.setdefault(h, []).append((o, x))
@@ -642,10 +645,31 @@ def refine_relay(relay, times):
     for h, os_ in groups.items():
         r_h = (1 + sum(x for _, x in os_)) / max(times[h], 1e-9)
         r_o = sum((1 - x) / max(times[o], 1e-9) for o, x in os_) / len(os_)
-        x = (r_h - r_o) / (r_h + len(os_) * r_o)
-        pairs += [(o, h, round(min(0.45, max(0.0, x)), 3)) for o, _ in os_]
-    return dict(relay, pairs=pairs, first_pass=relay["pairs"],
-                first_pass_times_s=[round(t, 3) for t in times])
+        target = (r_h - r_o) / (r_h + len(os_) * r_o)
+        pairs += [(o, h, round(min(0.45, max(0.0, x + damping * (target - x))), 3)) for o, x in os_]
+    return dict(relay, pairs=pairs)
+
+
+def tune_relay(relay, base_times, measure, arm, passes=3, damping=0.6):
+    """Plays the relay plan against the clock: arm it, time one step on every
+    rank (`measure` returns the gathered per-rank times), refine, and repeat;
+    then keep whichever plan had the smallest slowest-rank time, the plan
+    without relay (`base_times`) included. So the relay never makes a box
+    slower than it measured without it."""
+    best = (max(base_times), dict(relay, pairs=[]))
+    history = [{"pairs": [], "times_s": [round(t, 3) for t in base_times]}]
+    plan = relay
+    for it in range(passes if relay["mode"] == "auto" else 1):
+        arm(plan)
+        times = measure()
+        history.append({"pairs": plan["pairs"], "times_s": [round(t, 3) for t in times]})
+        if max(times) < best[0]:
+            best = (max(times), plan)
+        if relay["mode"] == "auto":
+            plan = refine_relay(plan, times, damping)
+    chosen = best[1] if relay["mode"] == "auto" else plan
+    arm(chosen)
+    return dict(chosen, history=history)
 
 
 def sum_stats(stats, sum_over_ranks):
@@ -1051,17 +1075,16 @@ def run_configs2(lz, torch, W, dev, tmp, rank, world, barrier, max_over_ranks, s
         step()
         warm_ms, payload = step()
         if use_relay:
-            relay = relay_plan(gather(round(payload / (warm_ms * 1e-3) / 1e9, 3)), relay_mode)
-            helper_of = {o: (h, sh) for o, h, sh in relay["pairs"]}
-            if rank in helper_of:
-                eng.set_relay(sock(helper_of[rank][0]), helper_of[rank][1])
-            if relay["pairs"] and relay_mode == "auto":
-                times = gather(statistics.mean(step()[0] for _ in range(2)) * 1e-3)
-                relay = refine_relay(relay, times)
-                helper_of = {o: (h, sh) for o, h, sh in relay["pairs"]}
-                if rank in helper_of:
-                    eng.set_relay(sock(helper_of[rank][0]), helper_of[rank][1])
-            barrier()
+            warm = gather(warm_ms * 1e-3)
+            relay = relay_plan([round(payload / t / 1e9, 3) for t in warm], relay_mode)
+            if relay["pairs"]:
+                def arm(p):
+                    mine = {o: (h, sh) for o, h, sh in p["pairs"]}
+                    eng.set_relay(sock(mine[rank][0]) if rank in mine else "", mine[rank][1] if rank in mine else 0.0)
+                    barrier()
+
+                relay = tune_relay(relay, warm, lambda: gather(statistics.mean(step()[0] for _ in range(2)) * 1e-3),
+                                   arm)
         ms = [step()[0] for _ in range(steps)]
         barrier()  # a helper must outlive its owners' requests
     finally:

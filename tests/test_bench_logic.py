@@ -60,3 +60,15 @@ def test_refine_moves_toward_equal_times():
     # the helper finishes last: the share must shrink
     refined = bench.refine_relay(plan, [2.8, 2.0, 2.0, 2.3])
     assert refined["pairs"][0][2] < 0.14
+
+
+def test_tune_relay_never_keeps_a_slower_plan():
+    """If every relayed plan measures slower than no relay, the relay goes off."""
+    armed = []
+    plan = bench.relay_plan([27.0, 27.0, 44.0, 44.0], "auto")
+    base = [1 / 27.0, 1 / 27.0, 1 / 44.0, 1 / 44.0]
+    res = bench.tune_relay(plan, base, measure=lambda: [0.1, 0.1, 0.1, 0.1], arm=armed.append)
+    assert res["pairs"] == [] and armed[-1]["pairs"] == []
+    # and keeps a plan that beats it
+    res = bench.tune_relay(plan, base, measure=lambda: [0.03, 0.03, 0.03, 0.03], arm=armed.append)
+    assert res["pairs"] and armed[-1]["pairs"] == res["pairs"]
