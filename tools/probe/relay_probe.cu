@@ -88,6 +88,36 @@ int main(int argc, char** argv) {
   if (can) {
     run("k", [&] { kern(0, bytes); }, bytes);
     run("ak", [&] { ce(sa, A, 0, bytes / 2); kern(bytes / 2, bytes / 2); }, bytes);
+    // copy engines only: A's memory -> B's HBM over NVLink (D2D), then B's
+    // HBM -> host over B's link, two chunks in flight on two streams
+    CK(cudaSetDevice(B));
+    void* stage = nullptr;
+    CK(cudaMalloc(&stage, 2 * chunk));
+    cudaStream_t sb2;
+    CK(cudaStreamCreateWithFlags(&sb2, cudaStreamNonBlocking));
+    cudaEvent_t in_done[2], out_done[2];
+    for (int k = 0; k < 2; ++k) {
+      CK(cudaEventCreateWithFlags(&in_done[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&out_done[k], cudaEventDisableTiming));
+      CK(cudaEventRecord(out_done[k], sb));
+    }
+    auto dd = [&](size_t off, size_t len) {
+      CK(cudaSetDevice(B));
+      int k = 0;
+      for (size_t o = 0; o < len; o += chunk, k ^= 1) {
+        const size_t n = std::min(chunk, len - o);
+        char* st = static_cast<char*>(stage) + k * chunk;
+        CK(cudaStreamWaitEvent(sb2, out_done[k], 0));
+        CK(cudaMemcpyAsync(st, static_cast<char*>(src) + off + o, n, cudaMemcpyDefault, sb2));
+        CK(cudaEventRecord(in_done[k], sb2));
+        CK(cudaStreamWaitEvent(sb, in_done[k], 0));
+        CK(cudaMemcpyAsync(static_cast<char*>(host) + off + o, st, n, cudaMemcpyDeviceToHost, sb));
+        CK(cudaEventRecord(out_done[k], sb));
+      }
+    };
+    run("dd", [&] { dd(0, bytes); }, bytes);
+    run("add", [&] { ce(sa, A, 0, bytes / 2); dd(bytes / 2, bytes / 2); }, bytes);
+    CK(cudaStreamSynchronize(sb2));
   }
   return 0;
 }
