@@ -204,6 +204,7 @@ typedef struct lzckpt_engine_config {
   const char* relay_peer_socket;    /* owner: delegate to the helper listening here */
   double relay_share;               /* fraction of each shard file's payload (0 = off) */
   uint64_t relay_min_entry;
+  int relay_kernel_route;           /* helper: 1 = SM gather kernel, 0 = copy engines (default) */
 } lzckpt_engine_config;
 void lzckpt_engine_config_defaults(lzckpt_engine_config* c);
 

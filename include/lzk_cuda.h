@@ -170,6 +170,9 @@ int lzk_ce_copy_d2h(lzk_stream* s, const lzk_copy_desc* d, uint32_t n);
 /* Restore direction: pinned host -> device. */
 int lzk_scatter_h2d(lzk_stream* s, const lzk_copy_desc* d, uint32_t n, uint32_t max_ctas);
 int lzk_ce_copy_h2d(lzk_stream* s, const lzk_copy_desc* d, uint32_t n);
+/* Device-to-device copy-engine variant (also peer memory opened through IPC:
+ * the uplink relay pulls a peer's tensors over NVLink this way). */
+int lzk_ce_copy_d2d(lzk_stream* s, const lzk_copy_desc* d, uint32_t n);
 /* Device-to-device multi-tensor gather (same kernel, device destination). */
 int lzk_gather_d2d(lzk_stream* s, const lzk_copy_desc* d, uint32_t n, uint32_t max_ctas);
 

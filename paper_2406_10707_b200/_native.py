@@ -54,7 +54,8 @@ class EngineConfigC(C.Structure):
                 ("force_kernel", i32), ("force_copy_engine", i32), ("hugepages", i32),
                 ("flush_discard", i32), ("stream_segment_bytes", u64), ("flush_hash_only", i32),
                 ("relay_serve_socket", cp), ("relay_staging_bytes", u64), ("relay_ctas", u32),
-                ("relay_peer_socket", cp), ("relay_share", f64), ("relay_min_entry", u64)]
+                ("relay_peer_socket", cp), ("relay_share", f64), ("relay_min_entry", u64),
+                ("relay_kernel_route", i32)]
 
 
 class IpcHandleC(C.Structure):
@@ -222,6 +223,7 @@ DEVICE_SYMBOLS = [
     ("lzk_ce_copy_d2h", i32, [vp, P(CopyDescC), u32]),
     ("lzk_scatter_h2d", i32, [vp, P(CopyDescC), u32, u32]),
     ("lzk_ce_copy_h2d", i32, [vp, P(CopyDescC), u32]),
+    ("lzk_ce_copy_d2d", i32, [vp, P(CopyDescC), u32]),
     ("lzk_gather_d2d", i32, [vp, P(CopyDescC), u32, u32]),
     ("lzk_fnv1a64_batch", i32, [vp, P(HashDescC), u32, u32]),
     ("lzk_fnv1a64_continue", i32, [vp, P(HashDescC), u32, u32]),

@@ -489,6 +489,7 @@ void lzckpt_engine_config_defaults(lzckpt_engine_config* c) {
   c->relay_peer_socket = nullptr;
   c->relay_share = 0;
   c->relay_min_entry = d.relay.min_entry;
+  c->relay_kernel_route = d.relay.copy_engines ? 0 : 1;
 }
 
 int lzckpt_engine_create(const lzckpt_engine_config* c, const lzckpt_topology* topo, uint32_t rank_dp,
@@ -522,6 +523,7 @@ int lzckpt_engine_create(const lzckpt_engine_config* c, const lzckpt_topology* t
     cfg.relay.peer_socket = c->relay_peer_socket ? c->relay_peer_socket : "";
     cfg.relay.share = c->relay_share;
     cfg.relay.min_entry = c->relay_min_entry;
+    cfg.relay.copy_engines = c->relay_kernel_route == 0;
     auto h = std::make_unique<lzckpt_engine>();
     h->topo = to_topo(topo);
     h->e = std::make_unique<Engine>(std::move(cfg), h->topo, RankCoord{rank_dp, rank_pp, rank_tp});

@@ -907,6 +907,10 @@ int lzk_ce_copy_h2d(lzk_stream* s, const lzk_copy_desc* d, uint32_t n) {
   return ce_copy(s, d, n, cudaMemcpyHostToDevice);
 }
 
+int lzk_ce_copy_d2d(lzk_stream* s, const lzk_copy_desc* d, uint32_t n) {
+  return ce_copy(s, d, n, cudaMemcpyDeviceToDevice);
+}
+
 int lzk_fill_splitmix(lzk_stream* s, void* dev, uint64_t bytes, uint64_t seed, uint64_t leaf) {
   if (!s) return fail(LZK_ERR_INVALID, "null stream");
   if (bytes == 0) return LZK_OK;

@@ -156,7 +156,8 @@ Engine::Engine(EngineConfig config, ParallelTopology topo, RankCoord rank)
   }
   if (!config_.relay.serve_socket.empty()) {
     relay_server_ = std::make_unique<detail::RelayServer>(transfers_.device(), config_.relay.serve_socket,
-                                                          config_.relay.staging_bytes, config_.relay.ctas);
+                                                          config_.relay.staging_bytes, config_.relay.ctas,
+                                                          config_.relay.copy_engines);
   }
   if (!config_.relay.peer_socket.empty() && config_.relay.share > 0) set_relay(config_.relay.peer_socket, config_.relay.share);
 }

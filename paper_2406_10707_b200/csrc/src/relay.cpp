@@ -130,14 +130,17 @@ struct RelayServer::Request {
   std::vector<RelayEntry> entries;
 };
 
-RelayServer::RelayServer(int device, std::string socket_path, uint64_t staging_bytes, uint32_t ctas)
+RelayServer::RelayServer(int device, std::string socket_path, uint64_t staging_bytes, uint32_t ctas,
+                         bool copy_engines)
     : device_(device),
       path_(std::move(socket_path)),
       chunk_(std::clamp<uint64_t>(staging_bytes / 4, 1ull << 20, 256ull << 20) & ~uint64_t(4095)),
-      ctas_(ctas ? ctas : 4) {
+      ctas_(ctas ? ctas : 4),
+      copy_engines_(copy_engines) {
   check(lzk_set_device(device_), "relay server: device");
   check(lzk_stream_create(device_, 0, &stream_), "relay server: stream");
   check(lzk_stream_create(device_, 0, &hash_stream_), "relay server: hash stream");
+  if (copy_engines_) check(lzk_stream_create(device_, 0, &pull_stream_), "relay server: pull stream");
   const size_t slots = size_t(std::max<uint64_t>(2, staging_bytes / chunk_));
   for (size_t k = 0; k < slots; ++k) {
     void* p = nullptr;
@@ -146,6 +149,14 @@ RelayServer::RelayServer(int device, std::string socket_path, uint64_t staging_b
     lzk_event* e = nullptr;
     check(lzk_event_create(device_, 1, &e), "relay server: event");
     chunk_done_.push_back(e);
+    if (copy_engines_) {
+      void* d = nullptr;
+      check(lzk_dev_alloc(device_, chunk_, &d), "relay server: HBM staging");
+      dev_stage_.push_back(d);
+      lzk_event* pe = nullptr;
+      check(lzk_event_create(device_, 0, &pe), "relay server: event");
+      pulled_.push_back(pe);
+    }
   }
   listen_fd_ = ::socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
   if (listen_fd_ < 0) throw IoError("relay server: socket() failed");
@@ -174,7 +185,11 @@ RelayServer::~RelayServer() {
   ::unlink(path_.c_str());
   lzk_stream_sync(stream_);
   lzk_stream_sync(hash_stream_);
+  if (pull_stream_) lzk_stream_sync(pull_stream_);
   for (auto* e : chunk_done_) lzk_event_destroy(e);
+  for (auto* e : pulled_) lzk_event_destroy(e);
+  for (void* d : dev_stage_) lzk_dev_free(device_, d);
+  if (pull_stream_) lzk_stream_destroy(pull_stream_);
   for (auto& [k, e] : events_) lzk_event_destroy(e);
   for (auto* p : staging_) lzk_host_free(p);
   if (digests_) lzk_host_free(digests_);
@@ -286,6 +301,7 @@ void RelayServer::handle(int fd, Request& r) {
         it = events_.emplace(key, e).first;
       }
       check(lzk_stream_wait_event(stream_, it->second), "relay: producer wait");
+      if (pull_stream_) check(lzk_stream_wait_event(pull_stream_, it->second), "relay: producer wait");
       if (r.flags & kRelayHash) check(lzk_stream_wait_event(hash_stream_, it->second), "relay: producer wait");
     }
     std::vector<uint64_t> sums;
@@ -347,7 +363,19 @@ void RelayServer::handle(int fd, Request& r) {
         }
       }
       if (!descs.empty()) {
-        check(lzk_gather_d2h(stream_, descs.data(), uint32_t(descs.size()), ctas_), "relay: gather");
+        if (copy_engines_) {
+          // pull over NVLink into HBM (D2D), then one DMA over this GPU's link;
+          // slot reuse is safe: retire(slot) above waited for its last DMA
+          auto* dst = static_cast<std::byte*>(dev_stage_[slot]);
+          for (auto& d : descs) d.dst = reinterpret_cast<uint64_t>(dst) + (d.dst - reinterpret_cast<uint64_t>(staging_[slot]));
+          check(lzk_ce_copy_d2d(pull_stream_, descs.data(), uint32_t(descs.size())), "relay: pull");
+          check(lzk_event_record(pulled_[slot], pull_stream_), "relay: event");
+          check(lzk_stream_wait_event(stream_, pulled_[slot]), "relay: pull wait");
+          const lzk_copy_desc out{reinterpret_cast<uint64_t>(dst), reinterpret_cast<uint64_t>(staging_[slot]), used};
+          check(lzk_ce_copy_d2h(stream_, &out, 1), "relay: push");
+        } else {
+          check(lzk_gather_d2h(stream_, descs.data(), uint32_t(descs.size()), ctas_), "relay: gather");
+        }
         check(lzk_event_record(chunk_done_[slot], stream_), "relay: event");
         slot_busy[slot] = true;
         total += used;

@@ -60,7 +60,11 @@ class RelayServer {
  public:
   // Serves owners on `socket_path` with the gather kernel on `device`
   // (`ctas` CTAs) through `staging_bytes` of pinned staging.
-  RelayServer(int device, std::string socket_path, uint64_t staging_bytes, uint32_t ctas);
+  // copy_engines: pull each chunk over NVLink into HBM staging with a D2D
+  // copy, then DMA it to host over this GPU's link (no SM time taken from
+  // the helper's training); false: the gather kernel reads the owner's HBM
+  // directly and stores to host (SM path).
+  RelayServer(int device, std::string socket_path, uint64_t staging_bytes, uint32_t ctas, bool copy_engines = true);
   ~RelayServer();
   RelayServer(const RelayServer&) = delete;
   RelayServer& operator=(const RelayServer&) = delete;
@@ -79,8 +83,12 @@ class RelayServer {
   const std::string path_;
   const uint64_t chunk_;
   const uint32_t ctas_;
+  const bool copy_engines_;
   int listen_fd_ = -1;
-  lzk_stream* stream_ = nullptr;       // gathers
+  lzk_stream* stream_ = nullptr;       // gathers / D2H
+  lzk_stream* pull_stream_ = nullptr;  // copy-engine route: D2D pulls over NVLink
+  std::vector<void*> dev_stage_;       // copy-engine route: HBM staging chunks
+  std::vector<lzk_event*> pulled_;
   lzk_stream* hash_stream_ = nullptr;  // entry checksums, beside the gathers
   std::vector<std::byte*> staging_;  // pinned, mapped chunks
   std::vector<lzk_event*> chunk_done_;

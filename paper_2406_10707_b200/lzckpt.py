@@ -563,6 +563,7 @@ class EngineConfig:
     relay_peer_socket: str = ""    # owner: delegate to the helper listening here
     relay_share: float = 0.0       # fraction of each shard file's payload
     relay_min_entry: int = 64 << 20
+    relay_kernel_route: bool = False  # helper: SM gather kernel instead of copy engines
 
     _STRINGS = ("checkpoint_root", "relay_serve_socket", "relay_peer_socket")
 
