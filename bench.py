@@ -323,7 +323,8 @@ def main_ours(args, rank, world, local_rank):
         pool_bytes = int(built.bytes * 1.01) + (256 << 20)
         cfg = lz.EngineConfig(checkpoint_root=os.path.join(tmp, "ckpt"), host_buffer_bytes=pool_bytes,
                               large_leaf_threshold=1 << 20, fsync_on_finalize=False, flush_discard=True,
-                              hugepages=True, device=dev, relay_serve_socket=sock(rank) if use_relay else "")
+                              hugepages=True, device=dev, relay_serve_socket=sock(rank) if use_relay else "",
+                              relay_kernel_route=args.relay_route == "kernel")
         t0 = time.time()
         try:
             eng = lz.Engine(cfg, built.topo, built.rank)
@@ -535,7 +536,7 @@ def main_ours(args, rank, world, local_rank):
                              "link_probes_per_rank": [{k: l[k] for k in ("dma_gbps", "sm_store_gbps", "numa_node")}
                                                       for l in links],
                              "algorithmic_bytes_per_step": payload},
-                "relay": dict(relay, stats=relay_stats) if relay["pairs"] else relay,
+                "relay": dict(relay, stats=relay_stats, route=args.relay_route) if relay["pairs"] else relay,
                 "stall": None if stall is None else dict(stall, durable=durable),
                 "streaming": streaming,
                 "matched": matched,
@@ -1112,6 +1113,9 @@ def main():
     ap.add_argument("--skip-configs2", action="store_true")
     ap.add_argument("--relay", default="auto", choices=["auto", "off", "force"],
                     help="uplink relay between ranks (N>1): auto = when the concurrent link probes are uneven")
+    ap.add_argument("--relay-route", default="ce", choices=["ce", "kernel"],
+                    help="helper's route: ce = NVLink D2D into HBM staging + DMA (no SM time), "
+                         "kernel = gather kernel reading the owner's HBM")
     args = ap.parse_args()
     if args.warmup < 3:
         log("[bench] warmup raised to 3 (timing rules)")

@@ -2,20 +2,21 @@
 // counterpart — the reference has one emulated link per rank).
 //
 // On hosts where several GPUs share one PCIe uplink, the slowest rank sets
-// every checkpoint's time. Measured (profiles/r02_relay_*): an
-// SM kernel on GPU B that reads GPU A's HBM over NVLink and stores to host
-// memory puts those bytes on B's link (a copy-engine DMA issued on B with A's
-// memory as source does not). The relay therefore runs in the HELPER's own
-// process (so its kernel shares the helper GPU with the helper's training
-// instead of being time-sliced against it):
+// every checkpoint's time. Measured (profiles/r02_relay_*): a
+// D2H DMA issued on GPU B with GPU A's memory as source does NOT use B's
+// link, but B's copy engines pulling A's memory into B's HBM (D2D over
+// NVLink) and then DMAing it to host do, at the full DMA rate; so does an SM
+// kernel on B reading A's HBM and storing to host, at a lower rate and with
+// SMs held. The relay runs in the HELPER's own process:
 //
 //   owner  capture() keeps a suffix of each shard file's large leaves out of
 //          its own D2H and sends them as a request: CUDA IPC handles of the
 //          leaves' allocations, the shard file and the leaves' file offsets,
 //          and an interprocess event recorded on the producer stream;
-//   helper waits for that event on its relay stream, gathers the leaves
-//          (lzk_gather_d2h reading the owner's HBM through IPC) into pinned
-//          staging on its own link, reports READ_DONE (the owner's lazy fence
+//   helper waits for that event on its relay streams, pulls the leaves
+//          from the owner's HBM through IPC into HBM staging (D2D), DMAs each
+//          staged chunk into pinned staging on its own link (or, SM route,
+//          gathers straight from the IPC source), reports READ_DONE (the owner's lazy fence
 //          needs it), then pwrites the bytes at their offsets in the owner's
 //          file, optionally hashes them (device FNV over the IPC source) and
 //          fsyncs, and reports PERSISTED with the entry checksums;
