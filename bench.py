@@ -1051,6 +1051,8 @@ def run_configs2(lz, torch, W, dev, tmp, rank, world, barrier, max_over_ranks, s
     planned from this block's own measured per-rank rates, as for the
     headline."""
     w = W.llama13b_shard(dp=8, rank=rank)
+    if not fits_host(int(max(gather(float(w.total_bytes))) * 1.03), world):
+        return {"skipped": f"{world} pinned rings of {w.total_bytes / 1e9:.1f} GB exceed 70 % of this host's RAM"}
     built = lz.build_workload(w.write_spec(os.path.join(tmp, "c3.spec")), dev)
     use_relay = relay_mode != "off"
     sock = lambda r: f"/tmp/lzk_relay_c3_{os.environ.get('MASTER_PORT', 'solo')}_{r}.sock"  # noqa: E731

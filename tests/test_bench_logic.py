@@ -72,3 +72,30 @@ def test_tune_relay_never_keeps_a_slower_plan():
     # and keeps a plan that beats it
     res = bench.tune_relay(plan, base, measure=lambda: [0.03, 0.03, 0.03, 0.03], arm=armed.append)
     assert res["pairs"] and armed[-1]["pairs"] == res["pairs"]
+
+
+def test_relay_plan_eight_ranks_two_uplink_classes():
+    """N=8 node where ranks 0-3 share uplinks in pairs and 4-7 have their own:
+    every owner gets exactly one helper, helpers are never owners, and every
+    share is within the cap."""
+    rates = [27.0, 27.2, 26.9, 27.1, 56.0, 55.5, 56.2, 55.8]
+    plan = bench.relay_plan(rates, "auto")
+    owners = [o for o, _, _ in plan["pairs"]]
+    helpers = {h for _, h, _ in plan["pairs"]}
+    assert sorted(owners) == [0, 1, 2, 3] and helpers == {4, 5, 6, 7}
+    assert not helpers & set(owners)
+    assert all(0 < x <= 0.45 for _, _, x in plan["pairs"])
+    assert bench.relay_plan(rates, "force")["pairs"] == [(0, 1, 0.3), (2, 3, 0.3), (4, 5, 0.3), (6, 7, 0.3)]
+
+
+def test_configs2_skips_when_host_ram_is_short(monkeypatch):
+    monkeypatch.setattr(bench, "fits_host", lambda b, w: False)
+
+    class W:
+        @staticmethod
+        def llama13b_shard(dp, rank):
+            class S:
+                total_bytes = 30 << 30
+            return S()
+    out = bench.run_configs2(None, None, W, 0, "/tmp", 0, 8, lambda: None, max, sum, lambda x: [x] * 8, None)
+    assert "skipped" in out
