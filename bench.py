@@ -393,13 +393,17 @@ def main_ours(args, rank, world, local_rank):
         if relay["pairs"]:
             tune_step = [30]
 
+            local = []
+
             def measure():
-                ts = []
+                ts, ds = [], []
                 for _ in range(2):
                     barrier()
                     dms, hms, _, _ = snap(tune_step[0])
                     tune_step[0] += 1
                     ts.append(max(dms, hms) * 1e-3)
+                    ds.append(dms * 1e-3)
+                local[:] = gather(statistics.mean(ds))  # the rank's own DMAs (device events)
                 return gather(statistics.mean(ts))
 
             def arm(p):
@@ -410,7 +414,7 @@ def main_ours(args, rank, world, local_rank):
                 barrier()
 
             base = [payload / (r * 1e9) for r in rank_rates]  # the hybrid sweep, no relay
-            relay = tune_relay(relay, base, measure, arm)
+            relay = tune_relay(relay, base, measure, arm, detail=lambda: {"local_dma_s": [round(t, 3) for t in local]})
             log(f"[bench] rank {rank}: uplink relay {relay}")
 
         # ---- timed region ----
@@ -651,7 +655,7 @@ def refine_relay(relay, times, damping=1.0):
     return dict(relay, pairs=pairs)
 
 
-def tune_relay(relay, base_times, measure, arm, passes=3, damping=0.6):
+def tune_relay(relay, base_times, measure, arm, passes=3, damping=0.6, detail=None):
     """Plays the relay plan against the clock: arm it, time one step on every
     rank (`measure` returns the gathered per-rank times), refine, and repeat;
     then keep whichever plan had the smallest slowest-rank time, the plan
@@ -663,7 +667,7 @@ def tune_relay(relay, base_times, measure, arm, passes=3, damping=0.6):
     for it in range(passes if relay["mode"] == "auto" else 1):
         arm(plan)
         times = measure()
-        history.append({"pairs": plan["pairs"], "times_s": [round(t, 3) for t in times]})
+        history.append(dict({"pairs": plan["pairs"], "times_s": [round(t, 3) for t in times]}, **(detail() if detail else {})))
         if max(times) < best[0]:
             best = (max(times), plan)
         if relay["mode"] == "auto":

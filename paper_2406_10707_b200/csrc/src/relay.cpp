@@ -128,6 +128,7 @@ struct RelayServer::Request {
   lzk_ipc_handle producer{};
   std::string path;
   std::vector<RelayEntry> entries;
+  std::chrono::steady_clock::time_point received{};
 };
 
 RelayServer::RelayServer(int device, std::string socket_path, uint64_t staging_bytes, uint32_t ctas,
@@ -245,6 +246,7 @@ void RelayServer::serve(int fd) {
     } catch (const std::exception&) {
       return;  // malformed: drop the connection
     }
+    r.received = std::chrono::steady_clock::now();
     std::lock_guard lk(mu_);
     if (stop_) return;
     handle(fd, r);
@@ -256,6 +258,7 @@ void RelayServer::serve(int fd) {
 // are gathered), READ_DONE once every read of the owner's memory is done,
 // then the remaining writes, fsync and PERSISTED.
 void RelayServer::handle(int fd, Request& r) {
+  const auto started = std::chrono::steady_clock::now();
   bool read_sent = false;
   auto reply = [&](uint32_t type, bool ok, const std::string& err, const std::vector<uint64_t>& sums) {
     Out o;
@@ -384,6 +387,15 @@ void RelayServer::handle(int fd, Request& r) {
     }
     check(lzk_stream_sync(stream_), "relay: reads");  // every read of the owner's memory is done
     check(lzk_stream_sync(hash_stream_), "relay: checksums");
+    if (trace_) {
+      using ms = std::chrono::duration<double, std::milli>;
+      const auto now = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[relay] dev %d req %llu: %.1f MB in %zu entries, queued %.2f ms, read %.2f ms (%.1f GB/s), idle before %.2f ms\n",
+                   device_, (unsigned long long)r.id, total / 1e6, n, ms(started - r.received).count(),
+                   ms(now - started).count(), total / 1e6 / std::max(1e-9, ms(now - started).count()),
+                   ms(started - last_done_).count());
+      last_done_ = now;
+    }
     if (r.flags & kRelayHash) sums.assign(digests_, digests_ + n);
     reply(kReadDone, true, "", {});
     read_sent = true;
@@ -442,7 +454,7 @@ void RelayClient::submit(const std::filesystem::path& file, uint32_t flags, cons
     std::lock_guard lk(mu_);
     if (broken_) throw IoError("relay: connection to the helper is lost");
     id = next_++;
-    pending_[id] = Pending{std::move(on_read), std::move(on_persisted), false};
+    pending_[id] = Pending{std::move(on_read), std::move(on_persisted), false, std::chrono::steady_clock::now()};
   }
   Out o;
   o.put(id);
@@ -503,6 +515,11 @@ void RelayClient::reader_loop() {
         if (type == kReadDone) {
           it->second.read = true;
           p.on_read = it->second.on_read;
+          if (trace_) {
+            std::fprintf(stderr, "[relay-owner] req %llu: READ_DONE %.2f ms after submit\n", (unsigned long long)id,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - it->second.sent)
+                             .count());
+          }
         } else {
           p = std::move(it->second);
           pending_.erase(it);

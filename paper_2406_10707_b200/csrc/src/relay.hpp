@@ -27,7 +27,9 @@
 // Transport: a Unix stream socket per helper, length-prefixed frames.
 #pragma once
 
+#include <chrono>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstdint>
 #include <filesystem>
 #include <functional>
@@ -99,6 +101,8 @@ class RelayServer {
   static constexpr size_t kMaxOpen = 4096;    // owners' allocations kept mapped
   std::set<std::string> opened_;
 
+  const bool trace_ = std::getenv("LZCKPT_TRACE") != nullptr;  // per-request timing on stderr
+  std::chrono::steady_clock::time_point last_done_{};
   mutable std::mutex mu_;  // one request at a time (the staging is shared)
   uint64_t bytes_ = 0;
   uint64_t requests_ = 0;
@@ -135,7 +139,9 @@ class RelayClient {
     ReadDone on_read;
     Persisted on_persisted;
     bool read = false;
+    std::chrono::steady_clock::time_point sent{};
   };
+  const bool trace_ = std::getenv("LZCKPT_TRACE") != nullptr;
   std::map<uint64_t, Pending> pending_;
   bool broken_ = false;
   std::thread reader_;
