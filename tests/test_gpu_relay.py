@@ -1,8 +1,9 @@
 """Uplink relay between two ranks (two processes, two GPUs): the owner (this
 process, cuda:0) delegates a suffix of each shard file's large leaves to a
 helper process on cuda:1, which reads them from the owner's HBM through CUDA
-IPC (NVLink) with its own gather kernel, stores them through its own PCIe
-link and writes them into the owner's files (relay.hpp). The files must be
+IPC (NVLink) with its copy engines (or its gather kernel), stores them through
+its own PCIe link and writes them into the owner's files (relay.hpp). Both
+helper routes run every test. The files must be
 byte-identical to the oracle's composition, with the header still written
 last by the owner; the capture stays ordered after the owner's trainer stream
 across the process boundary (interprocess event). Needs two GPUs; skipped
@@ -25,7 +26,8 @@ import os, sys, time
 sys.path.insert(0, os.environ["LZK_ROOT"])
 import paper_2406_10707_b200 as lz
 cfg = lz.EngineConfig(checkpoint_root=os.environ["LZK_TMP"], host_buffer_bytes=64 << 20, device=1,
-                      relay_serve_socket=os.environ["LZK_SOCK"], relay_staging_bytes=64 << 20)
+                      relay_serve_socket=os.environ["LZK_SOCK"], relay_staging_bytes=64 << 20,
+                      relay_kernel_route=os.environ.get("LZK_ROUTE") == "kernel")
 eng = lz.Engine(cfg, lz.ParallelTopology(1, 1, 1, 1, 1), lz.RankCoord())
 open(os.environ["LZK_SOCK"] + ".ready", "w").close()
 while not os.path.exists(os.environ["LZK_SOCK"] + ".stop"):
@@ -44,13 +46,15 @@ def workload():
     ], 1 << 20)
 
 
-@pytest.fixture
-def helper(tmp_path):
+@pytest.fixture(params=["ce", "kernel"])
+def helper(tmp_path, request):
+    """A helper process on cuda:1 serving the relay through its copy engines
+    (D2D pull into HBM staging, then DMA; the default) or its gather kernel."""
     torch = pytest.importorskip("torch")
     if torch.cuda.device_count() < 2:
         pytest.skip("the relay needs two GPUs (run with gpurun --gpus 2)")
     sock = str(tmp_path / "relay.sock")
-    env = dict(os.environ, LZK_ROOT=ROOT, LZK_TMP=str(tmp_path), LZK_SOCK=sock)
+    env = dict(os.environ, LZK_ROOT=ROOT, LZK_TMP=str(tmp_path), LZK_SOCK=sock, LZK_ROUTE=request.param)
     p = subprocess.Popen([sys.executable, "-c", HELPER], env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
                          text=True)
     t0 = time.time()
