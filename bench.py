@@ -399,7 +399,11 @@ def main_ours(args, rank, world, local_rank):
                 ts, ds = [], []
                 for _ in range(2):
                     barrier()
-                    dms, hms, _, _ = snap(tune_step[0])
+                    try:
+                        dms, hms, _, _ = snap(tune_step[0])
+                    except lz.Error as e:  # a failed relay: this plan scores inf, every rank stays in step
+                        log(f"[bench] rank {rank}: relay tuning step failed: {e}")
+                        dms = hms = float("inf")
                     tune_step[0] += 1
                     ts.append(max(dms, hms) * 1e-3)
                     ds.append(dms * 1e-3)
@@ -650,7 +654,8 @@ def refine_relay(relay, times, damping=1.0):
     for h, os_ in groups.items():
         r_h = (1 + sum(x for _, x in os_)) / max(times[h], 1e-9)
         r_o = sum((1 - x) / max(times[o], 1e-9) for o, x in os_) / len(os_)
-        target = (r_h - r_o) / (r_h + len(os_) * r_o)
+        den = r_h + len(os_) * r_o
+        target = (r_h - r_o) / den if den > 0 and math.isfinite(den) else 0.0  # a failed pass: back off
         pairs += [(o, h, round(min(0.45, max(0.0, x + damping * (target - x))), 3)) for o, x in os_]
     return dict(relay, pairs=pairs)
 
@@ -1090,8 +1095,16 @@ def run_configs2(lz, torch, W, dev, tmp, rank, world, barrier, max_over_ranks, s
                     eng.set_relay(sock(mine[rank][0]) if rank in mine else "", mine[rank][1] if rank in mine else 0.0)
                     barrier()
 
-                relay = tune_relay(relay, warm, lambda: gather(statistics.mean(step()[0] for _ in range(2)) * 1e-3),
-                                   arm)
+                def measure():
+                    ts = []
+                    for _ in range(2):
+                        try:
+                            ts.append(step()[0] * 1e-3)
+                        except lz.Error:  # a failed relay scores inf; the ranks stay in step
+                            ts.append(float("inf"))
+                    return gather(statistics.mean(ts))
+
+                relay = tune_relay(relay, warm, measure, arm)
         ms = [step()[0] for _ in range(steps)]
         barrier()  # a helper must outlive its owners' requests
     finally:

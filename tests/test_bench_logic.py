@@ -99,3 +99,13 @@ def test_configs2_skips_when_host_ram_is_short(monkeypatch):
             return S()
     out = bench.run_configs2(None, None, W, 0, "/tmp", 0, 8, lambda: None, max, sum, lambda x: [x] * 8, None)
     assert "skipped" in out
+
+
+def test_tune_relay_survives_a_failing_relay():
+    """A plan whose steps fail (measured as inf) is never kept, and refining
+    from it does not divide by zero."""
+    plan = bench.relay_plan([27.0, 27.0, 44.0, 44.0], "auto")
+    base = [1 / 27.0, 1 / 27.0, 1 / 44.0, 1 / 44.0]
+    armed = []
+    res = bench.tune_relay(plan, base, measure=lambda: [float("inf")] * 4, arm=armed.append)
+    assert res["pairs"] == [] and armed[-1]["pairs"] == []
