@@ -38,6 +38,7 @@ struct FlushConfig {
   // B200-host extensions
   unsigned threads = 0;              // worker pool size; 0 = auto (<= 8)
   uint64_t write_piece = 32ull << 20; // max bytes per pwrite job
+  unsigned max_writers = 0;          // concurrent pwrite jobs; 0 = no limit beyond `threads`
   // Host-memory tier only: no file is created, nothing is hashed or written;
   // a segment is released as soon as all of its bytes are resident. For
   // measuring the D2H snapshot stage on shards larger than local storage.
@@ -193,6 +194,7 @@ class FlushPipeline {
   uint64_t pending_files_ = 0;
   uint32_t callbacks_in_flight_ = 0;
   uint32_t busy_workers_ = 0;
+  uint32_t writers_ = 0;  // write jobs running (bounded by config_.max_writers)
   uint64_t bytes_written_ = 0;
   uint64_t files_persisted_ = 0;
   int64_t fail_after_ = -1;

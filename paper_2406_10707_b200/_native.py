@@ -55,7 +55,8 @@ class EngineConfigC(C.Structure):
                 ("flush_discard", i32), ("stream_segment_bytes", u64), ("flush_hash_only", i32),
                 ("relay_serve_socket", cp), ("relay_staging_bytes", u64), ("relay_ctas", u32),
                 ("relay_peer_socket", cp), ("relay_share", f64), ("relay_min_entry", u64),
-                ("relay_kernel_route", i32)]
+                ("relay_kernel_route", i32), ("flush_max_writers", u32),
+                ("flush_write_piece", u64)]
 
 
 class IpcHandleC(C.Structure):

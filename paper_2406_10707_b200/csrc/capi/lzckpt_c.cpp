@@ -490,6 +490,8 @@ void lzckpt_engine_config_defaults(lzckpt_engine_config* c) {
   c->relay_share = 0;
   c->relay_min_entry = d.relay.min_entry;
   c->relay_kernel_route = d.relay.copy_engines ? 0 : 1;
+  c->flush_max_writers = d.flush.max_writers;
+  c->flush_write_piece = d.flush.write_piece;
 }
 
 int lzckpt_engine_create(const lzckpt_engine_config* c, const lzckpt_topology* topo, uint32_t rank_dp,
@@ -524,6 +526,8 @@ int lzckpt_engine_create(const lzckpt_engine_config* c, const lzckpt_topology* t
     cfg.relay.share = c->relay_share;
     cfg.relay.min_entry = c->relay_min_entry;
     cfg.relay.copy_engines = c->relay_kernel_route == 0;
+    cfg.flush.max_writers = c->flush_max_writers;
+    if (c->flush_write_piece) cfg.flush.write_piece = c->flush_write_piece;
     auto h = std::make_unique<lzckpt_engine>();
     h->topo = to_topo(topo);
     h->e = std::make_unique<Engine>(std::move(cfg), h->topo, RankCoord{rank_dp, rank_pp, rank_tp});

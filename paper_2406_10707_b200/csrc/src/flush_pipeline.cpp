@@ -418,11 +418,21 @@ void FlushPipeline::worker_loop() {
   detail::bind_thread_to_node(pool_.numa_node());  // hashes and writes the ring's bytes
   std::unique_lock lk(mu_);
   for (;;) {
-    work_cv_.wait(lk, [&] { return stopping_ || !jobs_.empty(); });
+    // the oldest runnable job: a hash run, or a write while writers are below the cap
+    auto runnable = [&] {
+      const bool can_write = config_.max_writers == 0 || writers_ < config_.max_writers;
+      for (auto it = jobs_.begin(); it != jobs_.end(); ++it) {
+        if (it->hash || can_write) return it;
+      }
+      return jobs_.end();
+    };
+    work_cv_.wait(lk, [&] { return (stopping_ && jobs_.empty()) || runnable() != jobs_.end(); });
     if (jobs_.empty()) return;  // stopping and nothing left
-    Job j = jobs_.front();
-    jobs_.pop_front();
+    const auto pick = runnable();
+    Job j = *pick;
+    jobs_.erase(pick);
     ++busy_workers_;
+    if (!j.hash) ++writers_;
     FileRecord& f = files_.at(j.file);
     if (j.hash) {
       lk.unlock();
@@ -439,6 +449,7 @@ void FlushPipeline::worker_loop() {
         err = e.what();
       }
       lk.lock();
+      --writers_;
       if (!err.empty()) fail_locked(err);
       account(f, j.offset, j.offset + j.length);
       bytes_written_ += err.empty() ? j.length : 0;
