@@ -38,7 +38,12 @@ struct FlushConfig {
   // B200-host extensions
   unsigned threads = 0;              // worker pool size; 0 = auto (<= 8)
   uint64_t write_piece = 32ull << 20; // max bytes per pwrite job
-  unsigned max_writers = 0;          // concurrent pwrite jobs; 0 = no limit beyond `threads`
+  // Concurrent pwrite jobs; 0 = no limit beyond `threads`. The GPU boxes'
+  // virtio disk persists a C2 sample at 3.72 GB/s (median) with 3 writers
+  // against 3.35 with 8 (profiles/r02_flush_probe_writers.txt): fewer
+  // streams, and still one writer copying into its bounce buffer while
+  // another is in the kernel.
+  unsigned max_writers = 3;
   // Host-memory tier only: no file is created, nothing is hashed or written;
   // a segment is released as soon as all of its bytes are resident. For
   // measuring the D2H snapshot stage on shards larger than local storage.

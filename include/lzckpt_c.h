@@ -205,7 +205,7 @@ typedef struct lzckpt_engine_config {
   double relay_share;               /* fraction of each shard file's payload (0 = off) */
   uint64_t relay_min_entry;
   int relay_kernel_route;           /* helper: 1 = SM gather kernel, 0 = copy engines (default) */
-  uint32_t flush_max_writers;       /* concurrent pwrite jobs; 0 = no limit beyond flush_threads */
+  uint32_t flush_max_writers;       /* concurrent pwrite jobs (default 3); 0 = no limit beyond flush_threads */
   uint64_t flush_write_piece;       /* max bytes per pwrite job (default 32 MiB) */
 } lzckpt_engine_config;
 void lzckpt_engine_config_defaults(lzckpt_engine_config* c);

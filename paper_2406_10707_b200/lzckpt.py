@@ -564,7 +564,7 @@ class EngineConfig:
     relay_share: float = 0.0       # fraction of each shard file's payload
     relay_min_entry: int = 64 << 20
     relay_kernel_route: bool = False  # helper: SM gather kernel instead of copy engines
-    flush_max_writers: int = 0  # concurrent pwrite jobs (0: bounded by flush_threads only)
+    flush_max_writers: int = 3  # concurrent pwrite jobs (0: bounded by flush_threads only)
     flush_write_piece: int = 32 << 20  # max bytes per pwrite job
 
     _STRINGS = ("checkpoint_root", "relay_serve_socket", "relay_peer_socket")

@@ -22,14 +22,11 @@ import torch  # noqa: E402
 import paper_2406_10707_b200 as lz  # noqa: E402
 from paper_2406_10707_b200 import workloads as W  # noqa: E402
 
-CONFIGS = [  # (flush_threads, max_writers, write_piece MiB)
-    (0, 0, 32),   # the default
-    (0, 1, 64),
-    (0, 2, 32),
-    (0, 2, 64),
-    (0, 4, 32),
-    (0, 1, 128),
-]
+SETS = {  # (flush_threads, max_writers, write_piece MiB)
+    "wide": [(0, 0, 32), (0, 1, 64), (0, 2, 32), (0, 2, 64), (0, 4, 32), (0, 1, 128)],
+    "writers": [(0, 0, 32), (0, 3, 32), (0, 4, 32), (0, 6, 32), (0, 4, 64)],
+}
+CONFIGS = SETS[os.environ.get("LZK_FLUSH_SET", "wide")]
 
 
 def main():
