@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cerrno>
 #include <cstring>
 #include <exception>
@@ -23,6 +24,21 @@ void ck(int rc, const char* what) {
 }
 
 namespace {
+
+// Window reads: `read_threads()` concurrent preads of `read_piece()` bytes
+// (LZCKPT_READ_THREADS / LZCKPT_READ_PIECE_MB override, for tools/restore_probe.py).
+unsigned env_uint(const char* name, unsigned dflt) {
+  const char* v = std::getenv(name);
+  return v && std::atoi(v) > 0 ? unsigned(std::atoi(v)) : dflt;
+}
+unsigned read_threads() {
+  static const unsigned n = env_uint("LZCKPT_READ_THREADS", 8);
+  return n;
+}
+uint64_t read_piece() {
+  static const uint64_t n = uint64_t(env_uint("LZCKPT_READ_PIECE_MB", 64)) << 20;
+  return n;
+}
 
 // Runs fn(i) for i in [0, n) on up to `threads` threads.
 template <class Fn>
@@ -217,9 +233,9 @@ void FileStreamer::stream(int fd, const std::filesystem::path& path, uint64_t en
     Window& w = win_[i % kWindows];
     if (w.used) ck(lzk_event_sync(w.done), "file stream window reuse");
     const uint64_t off = uint64_t(i) * wsize, len = std::min(wsize, end - off);
-    const uint64_t piece = 64ull << 20;
+    const uint64_t piece = read_piece();
     const bool use_direct = dfd >= 0 && !mostly_cached(off, len);
-    parallel_for(size_t((len + piece - 1) / piece), 8, [&](size_t k) {
+    parallel_for(size_t((len + piece - 1) / piece), read_threads(), [&](size_t k) {
       const uint64_t o = uint64_t(k) * piece, n = std::min(piece, len - o);
       // O_DIRECT first (files written by the flush are usually not in the
       // page cache); windows are page-aligned and piece offsets 64 MiB
