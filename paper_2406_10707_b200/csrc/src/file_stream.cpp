@@ -25,19 +25,23 @@ void ck(int rc, const char* what) {
 
 namespace {
 
-// Window reads: `read_threads()` concurrent preads of `read_piece()` bytes
-// (LZCKPT_READ_THREADS / LZCKPT_READ_PIECE_MB override, for tools/restore_probe.py).
+// Window reads from the disk (O_DIRECT): 2 concurrent preads of 16 MiB. On
+// the GPU boxes' virtio disk that reads 6.0 GB/s against 4.0 for 8 x 64 MiB
+// (profiles/r02_disk_read_probe.txt) and restores a C2 sample at 3.55 GB/s
+// median against 3.25 (r02_restore_probe.txt). Windows already in the page
+// cache are memcpys: 8 threads x 64 MiB. LZCKPT_READ_THREADS /
+// LZCKPT_READ_PIECE_MB override the disk setting (tools/restore_probe.py).
 unsigned env_uint(const char* name, unsigned dflt) {
   const char* v = std::getenv(name);
   return v && std::atoi(v) > 0 ? unsigned(std::atoi(v)) : dflt;
 }
-unsigned read_threads() {
-  static const unsigned n = env_uint("LZCKPT_READ_THREADS", 8);
-  return n;
+unsigned read_threads(bool direct) {
+  static const unsigned n = env_uint("LZCKPT_READ_THREADS", 2);
+  return direct ? n : 8;
 }
-uint64_t read_piece() {
-  static const uint64_t n = uint64_t(env_uint("LZCKPT_READ_PIECE_MB", 64)) << 20;
-  return n;
+uint64_t read_piece(bool direct) {
+  static const uint64_t n = uint64_t(env_uint("LZCKPT_READ_PIECE_MB", 16)) << 20;
+  return direct ? n : 64ull << 20;
 }
 
 // Runs fn(i) for i in [0, n) on up to `threads` threads.
@@ -233,13 +237,13 @@ void FileStreamer::stream(int fd, const std::filesystem::path& path, uint64_t en
     Window& w = win_[i % kWindows];
     if (w.used) ck(lzk_event_sync(w.done), "file stream window reuse");
     const uint64_t off = uint64_t(i) * wsize, len = std::min(wsize, end - off);
-    const uint64_t piece = read_piece();
     const bool use_direct = dfd >= 0 && !mostly_cached(off, len);
-    parallel_for(size_t((len + piece - 1) / piece), read_threads(), [&](size_t k) {
+    const uint64_t piece = read_piece(use_direct);
+    parallel_for(size_t((len + piece - 1) / piece), read_threads(use_direct), [&](size_t k) {
       const uint64_t o = uint64_t(k) * piece, n = std::min(piece, len - o);
       // O_DIRECT first (files written by the flush are usually not in the
-      // page cache); windows are page-aligned and piece offsets 64 MiB
-      // multiples. The round-up of the last piece stays inside the window.
+      // page cache); windows are page-aligned and piece offsets multiples of
+      // the (MiB-sized) piece. The round-up of the last piece stays inside the window.
       if (!(use_direct && o + ((n + 4095) & ~uint64_t(4095)) <= w.cap && pread_direct(dfd, w.buf + o, n, off + o, end))) {
         pread_all(fd, w.buf + o, n, off + o, path);
       }
