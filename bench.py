@@ -397,6 +397,12 @@ def main_ours(args, rank, world, local_rank):
 
             def measure():
                 ts, ds = [], []
+                try:
+                    barrier()
+                    snap(tune_step[0])  # untimed: the helper opens the newly delegated allocations
+                except lz.Error as e:
+                    log(f"[bench] rank {rank}: relay warm-up step failed: {e}")
+                tune_step[0] += 1
                 for _ in range(2):
                     barrier()
                     try:
@@ -665,8 +671,12 @@ def tune_relay(relay, base_times, measure, arm, passes=3, damping=0.6, detail=No
     rank (`measure` returns the gathered per-rank times), refine, and repeat;
     then keep whichever plan had the smallest slowest-rank time, the plan
     without relay (`base_times`) included. So the relay never makes a box
-    slower than it measured without it."""
-    best = (max(base_times), dict(relay, pairs=[]))
+    slower than it measured without it. A relayed plan must beat "no relay"
+    by `margin` (2 %): within the step-to-step noise, no relay is kept.
+    `measure` should run an untimed step first: a new plan's first step
+    opens the owners' allocations in the helper (CUDA IPC), a one-time cost."""
+    margin = 0.02
+    best = (max(base_times) * (1 - margin), dict(relay, pairs=[]))
     history = [{"pairs": [], "times_s": [round(t, 3) for t in base_times]}]
     plan = relay
     for it in range(passes if relay["mode"] == "auto" else 1):
@@ -1085,7 +1095,8 @@ def run_configs2(lz, torch, W, dev, tmp, rank, world, barrier, max_over_ranks, s
     relay = {"mode": "off", "pairs": []}
     try:
         step()
-        warm_ms, payload = step()
+        warm_runs = [step() for _ in range(2)]
+        warm_ms, payload = statistics.mean(r[0] for r in warm_runs), warm_runs[0][1]
         if use_relay:
             warm = gather(warm_ms * 1e-3)
             relay = relay_plan([round(payload / t / 1e9, 3) for t in warm], relay_mode)
@@ -1097,9 +1108,11 @@ def run_configs2(lz, torch, W, dev, tmp, rank, world, barrier, max_over_ranks, s
 
                 def measure():
                     ts = []
-                    for _ in range(2):
+                    for k in range(3):  # the first step is untimed (IPC opens in the helper)
                         try:
-                            ts.append(step()[0] * 1e-3)
+                            ms = step()[0]
+                            if k:
+                                ts.append(ms * 1e-3)
                         except lz.Error:  # a failed relay scores inf; the ranks stay in step
                             ts.append(float("inf"))
                     return gather(statistics.mean(ts))

@@ -109,3 +109,14 @@ def test_tune_relay_survives_a_failing_relay():
     armed = []
     res = bench.tune_relay(plan, base, measure=lambda: [float("inf")] * 4, arm=armed.append)
     assert res["pairs"] == [] and armed[-1]["pairs"] == []
+
+
+def test_tune_relay_needs_a_margin_over_no_relay():
+    """A relayed plan within 2 % of "no relay" is noise: no relay is kept."""
+    plan = bench.relay_plan([57.0, 39.3], "auto")
+    base = [0.537, 0.780]
+    armed = []
+    res = bench.tune_relay(plan, base, measure=lambda: [0.537, 0.777], arm=armed.append)
+    assert res["pairs"] == [] and armed[-1]["pairs"] == []
+    res = bench.tune_relay(plan, base, measure=lambda: [0.60, 0.70], arm=armed.append)
+    assert res["pairs"]
