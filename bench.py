@@ -616,7 +616,7 @@ class PcieSampler:
 
 def relay_plan(rates, mode):
     """Uplink relay pairs from the ranks' snapshot rates measured all at once.
-    Ranks well below the fastest (< 80 %) are owners; ranks at >= 90 % of it
+    Ranks below 92 % of the fastest are owners; ranks at >= 95 % of it
     are helpers; owners are dealt to helpers round-robin (slowest first). A
     helper h with k owners of mean rate r_o takes share x of each, chosen so
     that all finish together: (1 - x) / r_o = (1 + k x) / r_h, damped by 10 %
@@ -630,8 +630,10 @@ def relay_plan(rates, mode):
         out["pairs"] = [(r, r + 1, 0.3) for r in range(0, n - 1, 2)]
         return out
     top = max(rates)
-    owners = sorted((r for r in range(n) if rates[r] < 0.8 * top), key=lambda r: rates[r])
-    helpers = sorted((r for r in range(n) if rates[r] >= 0.9 * top), key=lambda r: -rates[r])
+    # (tune_relay keeps "no relay" unless a plan measures 2 % faster, so a
+    # marginal owner costs tuning steps, never throughput)
+    owners = sorted((r for r in range(n) if rates[r] < 0.92 * top), key=lambda r: rates[r])
+    helpers = sorted((r for r in range(n) if rates[r] >= 0.95 * top), key=lambda r: -rates[r])
     if not owners or not helpers:
         return out
     groups = {h: [] for h in helpers}

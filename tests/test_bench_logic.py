@@ -120,3 +120,11 @@ def test_tune_relay_needs_a_margin_over_no_relay():
     assert res["pairs"] == [] and armed[-1]["pairs"] == []
     res = bench.tune_relay(plan, base, measure=lambda: [0.60, 0.70], arm=armed.append)
     assert res["pairs"]
+
+
+def test_relay_plan_mildly_uneven_pair():
+    """57.0 vs 48.9 GB/s (a 2-GPU box seen in the pool): rank 1 hands ~7 % to rank 0."""
+    plan = bench.relay_plan([57.0, 48.9], "auto")
+    assert [(o, h) for o, h, _ in plan["pairs"]] == [(1, 0)]
+    assert 0.04 < plan["pairs"][0][2] < 0.1
+    assert bench.relay_plan([57.0, 54.0], "auto")["pairs"] == []
