@@ -30,7 +30,7 @@ namespace {
 // (profiles/r02_disk_read_probe.txt) and restores a C2 sample at 3.55 GB/s
 // median against 3.25 (r02_restore_probe.txt). Windows already in the page
 // cache are memcpys: 8 threads x 64 MiB. LZCKPT_READ_THREADS /
-// LZCKPT_READ_PIECE_MB override the disk setting (tools/restore_probe.py).
+// LZCKPT_READ_PIECE_MB override the disk setting (tools/restore_read_probe.py).
 unsigned env_uint(const char* name, unsigned dflt) {
   const char* v = std::getenv(name);
   return v && std::atoi(v) > 0 ? unsigned(std::atoi(v)) : dflt;
