@@ -69,17 +69,39 @@ int main(int argc, char** argv) {
     CK(cudaStreamSynchronize(sa));
     CK(cudaStreamSynchronize(sb));
   };
+  // per-stream elapsed time (events on A's and B's streams around fn)
+  cudaEvent_t a0, a1, b0, b1;
+  CK(cudaSetDevice(A));
+  CK(cudaEventCreate(&a0));
+  CK(cudaEventCreate(&a1));
+  CK(cudaSetDevice(B));
+  CK(cudaEventCreate(&b0));
+  CK(cudaEventCreate(&b1));
   auto run = [&](const char* name, auto fn, size_t moved) {
     fn();
     sync();  // warm-up
     double best = 0;
+    float ta = 0, tb = 0;
     for (int r = 0; r < 4; ++r) {
+      CK(cudaSetDevice(A));
+      CK(cudaEventRecord(a0, sa));
+      CK(cudaSetDevice(B));
+      CK(cudaEventRecord(b0, sb));
       const double t0 = now();
       fn();
+      CK(cudaSetDevice(A));
+      CK(cudaEventRecord(a1, sa));
+      CK(cudaSetDevice(B));
+      CK(cudaEventRecord(b1, sb));
       sync();
-      best = std::max(best, moved / (now() - t0) / 1e9);
+      const double gbps = moved / (now() - t0) / 1e9;
+      if (gbps > best) {
+        best = gbps;
+        CK(cudaEventElapsedTime(&ta, a0, a1));
+        CK(cudaEventElapsedTime(&tb, b0, b1));
+      }
     }
-    std::printf("%-4s %8.2f GB/s\n", name, best);
+    std::printf("%-8s %8.2f GB/s   (A stream %.1f ms, B stream %.1f ms)\n", name, best, ta, tb);
   };
   run("a", [&] { ce(sa, A, 0, bytes); }, bytes);
   run("b", [&] { ce(sb, B, 0, bytes); }, bytes);
@@ -92,7 +114,7 @@ int main(int argc, char** argv) {
     // HBM -> host over B's link, two chunks in flight on two streams
     CK(cudaSetDevice(B));
     void* stage = nullptr;
-    CK(cudaMalloc(&stage, 2 * chunk));
+    CK(cudaMalloc(&stage, 2 * chunk));  // two slots of the largest chunk size
     cudaStream_t sb2;
     CK(cudaStreamCreateWithFlags(&sb2, cudaStreamNonBlocking));
     cudaEvent_t in_done[2], out_done[2];
@@ -101,11 +123,12 @@ int main(int argc, char** argv) {
       CK(cudaEventCreateWithFlags(&out_done[k], cudaEventDisableTiming));
       CK(cudaEventRecord(out_done[k], sb));
     }
-    auto dd = [&](size_t off, size_t len) {
+    auto dd = [&](size_t off, size_t len, size_t step = 0) {
+      if (step == 0) step = chunk;
       CK(cudaSetDevice(B));
       int k = 0;
-      for (size_t o = 0; o < len; o += chunk, k ^= 1) {
-        const size_t n = std::min(chunk, len - o);
+      for (size_t o = 0; o < len; o += step, k ^= 1) {
+        const size_t n = std::min(step, len - o);
         char* st = static_cast<char*>(stage) + k * chunk;
         CK(cudaStreamWaitEvent(sb2, out_done[k], 0));
         CK(cudaMemcpyAsync(st, static_cast<char*>(src) + off + o, n, cudaMemcpyDefault, sb2));
@@ -117,6 +140,16 @@ int main(int argc, char** argv) {
     };
     run("dd", [&] { dd(0, bytes); }, bytes);
     run("add", [&] { ce(sa, A, 0, bytes / 2); dd(bytes / 2, bytes / 2); }, bytes);
+    // the same with smaller pull/push chunks: the NVLink pull of A's memory
+    // runs in shorter bursts (does A's own DMA lose less?)
+    for (size_t mib : {64, 16, 4}) {
+      char name[16];
+      std::snprintf(name, sizeof name, "add%zu", mib);
+      run(name, [&] { ce(sa, A, 0, bytes / 2); dd(bytes / 2, bytes / 2, mib << 20); }, bytes);
+    }
+    // A's own DMA alone over the same half, for the split
+    run("a_half", [&] { ce(sa, A, 0, bytes / 2); }, bytes / 2);
+    run("dd_half", [&] { dd(bytes / 2, bytes / 2); }, bytes / 2);
     CK(cudaStreamSynchronize(sb2));
   }
   return 0;
