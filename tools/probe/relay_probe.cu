@@ -147,6 +147,14 @@ int main(int argc, char** argv) {
       std::snprintf(name, sizeof name, "add%zu", mib);
       run(name, [&] { ce(sa, A, 0, bytes / 2); dd(bytes / 2, bytes / 2, mib << 20); }, bytes);
     }
+    // the pull alone (A's memory -> B's HBM): ~NVLink rate, or a PCIe rate
+    // when the peer path is not NVLink
+    run("pull", [&] {
+      CK(cudaSetDevice(B));
+      for (size_t o = 0; o < bytes; o += chunk) {
+        CK(cudaMemcpyAsync(stage, static_cast<char*>(src) + o, chunk, cudaMemcpyDefault, sb));
+      }
+    }, bytes);
     // A's own DMA alone over the same half, for the split
     run("a_half", [&] { ce(sa, A, 0, bytes / 2); }, bytes / 2);
     run("dd_half", [&] { dd(bytes / 2, bytes / 2); }, bytes / 2);
