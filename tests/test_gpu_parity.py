@@ -34,6 +34,8 @@ VARIANTS = {
     "durable": {"fsync_on_finalize": True},
     "durable-streaming": {"fsync_on_finalize": True, "stream_segment_bytes": 1_000_003,
                           "host_buffer_bytes": 3_000_009, "chunk_quantum": 262_147},
+    # one writer at a time, odd small pieces (FlushConfig::max_writers / write_piece)
+    "durable-one-writer": {"fsync_on_finalize": True, "flush_max_writers": 1, "flush_write_piece": 1_048_576 + 4096},
 }
 
 
