@@ -114,3 +114,63 @@ def test_two_rank_distributed_commit(tmp_path):
     paths = [f["path"] for f in m["steps"][0]["files"]]
     assert paths == sorted(paths) and len(paths) == 4
     assert {f["length"] for f in m["steps"][0]["files"]} == {100, 101, 200, 201}
+
+
+def _relay_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+
+    def gather(x):
+        g = [None] * world
+        dist.all_gather_object(g, x)
+        return g
+
+    my_rate = [57.0, 45.0][rank]
+    rates = gather(my_rate)
+    plan = bench.relay_plan(rates, "auto")
+    armed = {"pairs": []}
+
+    def arm(p):
+        armed["pairs"] = p["pairs"]
+        dist.barrier()
+
+    def measure():
+        # this rank's time under the armed plan: an owner moves (1 - x) of its
+        # shard, a helper 1 + x, at the rank's own rate
+        x_out = sum(x for o, _, x in armed["pairs"] if o == rank)
+        x_in = sum(x for _, h, x in armed["pairs"] if h == rank)
+        return gather((1 - x_out + x_in) / my_rate)
+
+    base = gather(1 / my_rate)
+    res = bench.tune_relay(plan, base, measure, arm)
+    out.put((rank, res["pairs"], armed["pairs"]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_relay_tuning_agrees():
+    """bench.py's relay planning at N=2 over gloo: every rank derives the same
+    plan from the gathered rates, tunes it against gathered per-rank times, and
+    arms the same final plan (the slower rank hands a share to the faster)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_relay_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        rank, pairs, armed = q.get(timeout=240)
+        res[rank] = (pairs, armed)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0] == res[1]
+    pairs, armed = res[0]
+    assert pairs == armed and [(o, h) for o, h, _ in pairs] == [(1, 0)]
+    x = pairs[0][2]
+    assert 0.05 < x < 0.2  # near the equalising share (57 - 45) / (57 + 45) = 0.118
