@@ -22,6 +22,8 @@
 #pragma once
 
 #include <atomic>
+#include <chrono>
+#include <cstdlib>
 #include <condition_variable>
 #include <cstddef>
 #include <cstdint>
@@ -261,6 +263,8 @@ class TransferEngine {
     bool prologue = false;                 // the ticket's __meta__ is written on the device
     std::vector<InlineWatch> inline_watch;  // verdict at the first completed group
     std::vector<std::shared_ptr<const void>> inline_keep;  // until the first group completes
+    // LZCKPT_TRACE: host-side timeline of the ticket's device path
+    std::chrono::steady_clock::time_point t_submit{}, t_first_issue{}, t_last_issue{}, t_last_sync{};
   };
 
   void issuer_loop();
@@ -273,6 +277,7 @@ class TransferEngine {
   void give_event(lzk_event* e);
 
   HostBufferPool& pool_;
+  const bool trace_ = std::getenv("LZCKPT_TRACE") != nullptr;
   const ThrottledChannel channel_;
   SnapshotOptions opts_;
   int device_ = 0;

@@ -226,6 +226,7 @@ void TransferEngine::submit_copies(uint64_t ticket, std::vector<std::shared_ptr<
     std::lock_guard lk(mu_);
     if (stopping_) throw Error("submit_copies: engine is shutting down");
     auto& tp = tickets_[ticket];
+    if (trace_ && tp.t_submit == std::chrono::steady_clock::time_point{}) tp.t_submit = std::chrono::steady_clock::now();
     tp.expected += tasks.size();
     tp.unissued += groups.size();
     tp.tasks.insert(tp.tasks.end(), std::make_move_iterator(tasks.begin()), std::make_move_iterator(tasks.end()));
@@ -280,7 +281,7 @@ void TransferEngine::build_groups(const std::vector<std::shared_ptr<CopyTask>>& 
   uint64_t cur_bytes = 0;
   Segment seg;
   for (const auto& t : tasks) {
-    t->state.store(CopyState::Copying);
+    t->state.store(CopyState::Copying, std::memory_order_relaxed);  // published to the issuer under mu_
     if (seg.id != t->segment_id) seg = pool_.segment_info(t->segment_id);
     std::byte* dst = pool_base + seg.offset + t->dst_offset;
     const bool use_ce = o.force_copy_engine || (!o.force_kernel && t->length >= o.ce_threshold);
@@ -380,6 +381,10 @@ void TransferEngine::issuer_loop() {
       auto& tp = tickets_[g.ticket];
       --tp.unissued;
       tp.last_event = g.done;
+      if (trace_) {
+        tp.t_last_issue = std::chrono::steady_clock::now();
+        if (tp.t_first_issue == std::chrono::steady_clock::time_point{}) tp.t_first_issue = tp.t_last_issue;
+      }
       if (start) tp.start_event = start;
       stats_.groups += 1;
       stats_.kernel_launches += (g.kernel.size() + 959) / 960;
@@ -430,6 +435,16 @@ void TransferEngine::worker_loop() {
           if (lzk_event_elapsed_ms(tp.start_event, g.done, &ms) == LZK_OK) tp.device_ms = ms;
           give_event(tp.start_event);
           tp.start_event = nullptr;
+          if (trace_) {
+            using msd = std::chrono::duration<double, std::milli>;
+            const auto now = std::chrono::steady_clock::now();
+            std::fprintf(stderr,
+                         "[lzckpt transfer ms] ticket %llu: %llu tasks, submit->first issue %.3f, issue span %.3f, "
+                         "device %.3f, last issue->last sync %.3f, last sync->done %.3f\n",
+                         (unsigned long long)g.ticket, (unsigned long long)tp.expected,
+                         msd(tp.t_first_issue - tp.t_submit).count(), msd(tp.t_last_issue - tp.t_first_issue).count(),
+                         double(ms), msd(tp.t_last_sync - tp.t_last_issue).count(), msd(now - tp.t_last_sync).count());
+          }
         }
         if (tp.last_event == g.done) tp.last_event = nullptr;
         give_event(g.done);
@@ -465,6 +480,7 @@ void TransferEngine::run_device_group(Group& g) {
   };
   if (!g.host_after_device) host_copies();
   const bool device_ok = !g.issue_failed && lzk_event_sync(g.done) == LZK_OK;
+  const auto synced = std::chrono::steady_clock::now();
   if (g.host_after_device) host_copies();
   std::vector<char> torn(g.pieces.size(), 0);
   bool inline_torn = false;
@@ -474,6 +490,7 @@ void TransferEngine::run_device_group(Group& g) {
     // The prologue's inline gather ran before this group on the stream: its
     // verdict is due at the ticket's first completed group.
     auto& tp = tickets_[g.ticket];
+    tp.t_last_sync = synced;
     tp.inline_keep.clear();  // the prologue's gather ran before this group
     if (!tp.inline_watch.empty()) {
       for (const auto& w : tp.inline_watch) {
@@ -490,7 +507,7 @@ void TransferEngine::run_device_group(Group& g) {
       // A device fault leaves the bytes undefined: report the task torn so
       // the ticket fails and its files never gain a header.
       torn[i] = !device_ok || torn_verdict(*p.task);
-      p.task->state.store(torn[i] ? CopyState::Torn : CopyState::Done);
+      p.task->state.store(torn[i] ? CopyState::Torn : CopyState::Done, std::memory_order_release);
     }
   }
   if (inline_torn && torn_cb_) {
