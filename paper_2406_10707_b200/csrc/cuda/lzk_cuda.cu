@@ -29,7 +29,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdlib>
 #include <atomic>
 #include <cctype>
 #include <cstdint>
@@ -122,16 +121,12 @@ struct Desc {
   uint64_t tile_begin;  // exclusive prefix of tile counts
 };
 
-// The descriptor table travels in the kernel parameters (constant bank:
-// warp-uniform lookups are broadcast). CAP sets the parameter size.
-template <uint32_t CAP>
-struct DescBatchT {
+struct DescBatch {
   uint32_t n;
   uint32_t pad;
   uint64_t total_tiles;
-  Desc d[CAP];
+  Desc d[kMaxDescPerLaunch];
 };
-using DescBatch = DescBatchT<kMaxDescPerLaunch>;
 static_assert(sizeof(DescBatch) <= 31 * 1024, "kernel parameter budget");
 
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
@@ -272,9 +267,8 @@ __device__ __forceinline__ void copy_span(const uint8_t* src, uint8_t* dst, uint
 // descriptor, mis = dst & 127, so interior boundaries sit on 128-byte lines.
 // Each warp finds its descriptor by a warp-uniform binary search over the
 // tile prefix (broadcast constant-bank reads).
-template <uint32_t CAP>
 __global__ void __launch_bounds__(kThreads)
-    lzk_gather_kernel(const __grid_constant__ DescBatchT<CAP> batch) {
+    lzk_gather_kernel(const __grid_constant__ DescBatch batch) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint64_t warp = uint64_t(blockIdx.x) * kWarps + (threadIdx.x >> 5);
   const uint64_t nwarps = uint64_t(gridDim.x) * kWarps;
@@ -294,14 +288,17 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-template <uint32_t CAP>
-int launch_gather_cap(cudaStream_t stream, const lzk_copy_desc* d, uint32_t n, uint32_t max_ctas) {
-  thread_local DescBatchT<CAP> batch;
+int launch_gather(cudaStream_t stream, const lzk_copy_desc* d, uint32_t n, uint32_t max_ctas) {
+  if (n == 0) return LZK_OK;
+  if (d == nullptr) return fail(LZK_ERR_INVALID, "gather: null descriptor array");
+  if (max_ctas == 0) max_ctas = 4;  // 2 saturate the host link (profiles/r02_ctasweep.jsonl)
+  // Stack-allocating 31 KB is fine for host threads; keep it static per thread.
+  thread_local DescBatch batch;
   uint32_t i = 0;
   while (i < n) {
     batch.n = 0;
     uint64_t tiles = 0;
-    for (; i < n && batch.n < CAP; ++i) {
+    for (; i < n && batch.n < kMaxDescPerLaunch; ++i) {
       if (d[i].len == 0) continue;
       Desc& x = batch.d[batch.n++];
       x.src = d[i].src;
@@ -313,25 +310,12 @@ int launch_gather_cap(cudaStream_t stream, const lzk_copy_desc* d, uint32_t n, u
     if (batch.n == 0) continue;
     batch.total_tiles = tiles;
     uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>((tiles + kWarps - 1) / kWarps, max_ctas));
-    lzk_gather_kernel<CAP><<<grid, kThreads, 0, stream>>>(batch);
+    lzk_gather_kernel<<<grid, kThreads, 0, stream>>>(batch);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "lzk_gather_kernel launch");
     lzk_detail::launches.fetch_add(1, std::memory_order_relaxed);
   }
   return LZK_OK;
-}
-
-int launch_gather(cudaStream_t stream, const lzk_copy_desc* d, uint32_t n, uint32_t max_ctas) {
-  if (n == 0) return LZK_OK;
-  if (d == nullptr) return fail(LZK_ERR_INVALID, "gather: null descriptor array");
-  if (max_ctas == 0) max_ctas = 4;  // 2 saturate the host link (profiles/r02_ctasweep.jsonl)
-  static const uint32_t cap = [] {
-    const char* v = std::getenv("LZK_GATHER_CAP");  // launch-shape experiment (tools/cap_small.py)
-    return v ? uint32_t(std::atoi(v)) : kMaxDescPerLaunch;
-  }();
-  if (cap == 120) return launch_gather_cap<120>(stream, d, n, max_ctas);
-  if (cap == 240) return launch_gather_cap<240>(stream, d, n, max_ctas);
-  return launch_gather_cap<kMaxDescPerLaunch>(stream, d, n, max_ctas);
 }
 
 // ---------------------------------------------------------------------------
