@@ -206,6 +206,12 @@ class TransferEngine {
   // Device time of a completed ticket's snapshot (CUDA events on the snapshot
   // stream, first device op -> last completion); < 0 when not measured.
   double ticket_device_ms(uint64_t ticket) const;
+  // A capture that submits several files holds its ticket until the last is
+  // submitted, so that an early file completing first does not close the
+  // ticket's device time. Unheld tickets (direct submit_copies users) close
+  // whenever everything submitted so far has completed.
+  void hold(uint64_t ticket);
+  void seal(uint64_t ticket);
   const SnapshotOptions& options() const { return opts_; }
   // Changes the variant selection for subsequent submissions (device and
   // stream priority are fixed at construction).
@@ -265,6 +271,8 @@ class TransferEngine {
     std::vector<std::shared_ptr<const void>> inline_keep;  // until the first group completes
     // LZCKPT_TRACE: host-side timeline of the ticket's device path
     std::chrono::steady_clock::time_point t_submit{}, t_first_issue{}, t_last_issue{}, t_last_sync{};
+    bool held = false;                 // hold()/seal(): more files may still be submitted
+    lzk_event* final_event = nullptr;  // the last completed group's event, until device_ms is taken
   };
 
   void issuer_loop();
@@ -273,6 +281,7 @@ class TransferEngine {
   void run_paced_group(Group& g);
   void build_groups(const std::vector<std::shared_ptr<CopyTask>>& tasks, std::deque<Group>& out);
   void issue(Group& g);
+  void finalize_device_time(uint64_t ticket, TicketProgress& tp);
   lzk_event* take_event();
   void give_event(lzk_event* e);
 

@@ -504,6 +504,13 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
     share = relay_client_ ? relay_share_ : 0;
   }
   const bool relay = share > 0 && config_.copy_channel.bandwidth_Bps <= 0;
+  // the ticket's device time closes only after its last file is submitted
+  transfers_.hold(ticket->id_);
+  struct Seal {
+    TransferEngine& t;
+    uint64_t id;
+    ~Seal() { t.seal(id); }
+  } seal{transfers_, ticket->id_};
   for (auto& b : builds) {
     // Uplink relay: a suffix of the file's large region leaves, up to `share`
     // of its payload, goes to the helper (its bytes never enter this ring).

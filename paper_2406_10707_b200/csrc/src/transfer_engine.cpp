@@ -144,6 +144,10 @@ TransferEngine::~TransferEngine() {
   work_cv_.notify_all();
   if (worker_.joinable()) worker_.join();
   lzk_stream_destroy(stream_);
+  for (auto& [id, tp] : tickets_) {  // tickets never sealed (e.g. an aborted capture)
+    if (tp.start_event) lzk_event_destroy(tp.start_event);
+    if (tp.final_event) lzk_event_destroy(tp.final_event);
+  }
   for (lzk_event* e : free_events_) lzk_event_destroy(e);
 }
 
@@ -430,24 +434,16 @@ void TransferEngine::worker_loop() {
       if (tg.completed == tg.expected) tg.tasks.clear();  // drop region references (pieces point into them)
       if (g.done) {
         auto& tp = tickets_[g.ticket];
-        if (tp.completed == tp.expected && tp.start_event && tp.unissued == 0) {
-          float ms = -1;
-          if (lzk_event_elapsed_ms(tp.start_event, g.done, &ms) == LZK_OK) tp.device_ms = ms;
-          give_event(tp.start_event);
-          tp.start_event = nullptr;
-          if (trace_) {
-            using msd = std::chrono::duration<double, std::milli>;
-            const auto now = std::chrono::steady_clock::now();
-            std::fprintf(stderr,
-                         "[lzckpt transfer ms] ticket %llu: %llu tasks, submit->first issue %.3f, issue span %.3f, "
-                         "device %.3f, last issue->last sync %.3f, last sync->done %.3f\n",
-                         (unsigned long long)g.ticket, (unsigned long long)tp.expected,
-                         msd(tp.t_first_issue - tp.t_submit).count(), msd(tp.t_last_issue - tp.t_first_issue).count(),
-                         double(ms), msd(tp.t_last_sync - tp.t_last_issue).count(), msd(now - tp.t_last_sync).count());
-          }
-        }
         if (tp.last_event == g.done) tp.last_event = nullptr;
-        give_event(g.done);
+        if (tp.completed == tp.expected && tp.start_event && tp.unissued == 0) {
+          // everything submitted so far is done; a held ticket (a capture
+          // still submitting files) keeps the event until it is sealed
+          if (tp.final_event) give_event(tp.final_event);
+          tp.final_event = g.done;
+          if (!tp.held) finalize_device_time(g.ticket, tp);
+        } else {
+          give_event(g.done);
+        }
       }
     }
     progress_cv_.notify_all();
@@ -610,6 +606,40 @@ bool TransferEngine::ticket_complete(uint64_t ticket) const {
   std::lock_guard lk(mu_);
   auto it = tickets_.find(ticket);
   return it == tickets_.end() || it->second.completed == it->second.expected;
+}
+
+// Caller holds mu_; tp.final_event is the last completed group's event.
+void TransferEngine::finalize_device_time(uint64_t ticket, TicketProgress& tp) {
+  float ms = -1;
+  if (lzk_event_elapsed_ms(tp.start_event, tp.final_event, &ms) == LZK_OK) tp.device_ms = ms;
+  give_event(tp.start_event);
+  give_event(tp.final_event);
+  tp.start_event = nullptr;
+  tp.final_event = nullptr;
+  if (trace_) {
+    using msd = std::chrono::duration<double, std::milli>;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr,
+                 "[lzckpt transfer ms] ticket %llu: %llu tasks, submit->first issue %.3f, issue span %.3f, "
+                 "device %.3f, last issue->last sync %.3f, last sync->done %.3f\n",
+                 (unsigned long long)ticket, (unsigned long long)tp.expected,
+                 msd(tp.t_first_issue - tp.t_submit).count(), msd(tp.t_last_issue - tp.t_first_issue).count(),
+                 double(ms), msd(tp.t_last_sync - tp.t_last_issue).count(), msd(now - tp.t_last_sync).count());
+  }
+}
+
+void TransferEngine::hold(uint64_t ticket) {
+  std::lock_guard lk(mu_);
+  tickets_[ticket].held = true;
+}
+
+void TransferEngine::seal(uint64_t ticket) {
+  std::lock_guard lk(mu_);
+  auto& tp = tickets_[ticket];
+  tp.held = false;
+  if (tp.final_event && tp.start_event && tp.completed == tp.expected && tp.unissued == 0) {
+    finalize_device_time(ticket, tp);
+  }
 }
 
 double TransferEngine::ticket_device_ms(uint64_t ticket) const {
