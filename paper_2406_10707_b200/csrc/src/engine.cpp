@@ -552,10 +552,19 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
                    producer.ordered);
       b.larges.resize(own);
     }
-    // one allocation for the file's tasks; each task shares the block
+    // one allocation for the file's tasks; each task shares the block. Tasks
+    // are submitted in chunks as they are built, so that a file of many small
+    // leaves is already on the device while the rest of its tasks are made.
     auto block = std::make_shared<std::vector<CopyTask>>(1 + b.larges.size());
+    constexpr size_t kSubmitChunk = 1024;
     std::vector<std::shared_ptr<CopyTask>> tasks;
-    tasks.reserve(block->size());
+    tasks.reserve(std::min(block->size(), kSubmitChunk));
+    auto submit = [&] {
+      if (tasks.empty()) return;
+      transfers_.submit_copies(ticket->id_, std::move(tasks));
+      tasks.clear();
+      tasks.reserve(kSubmitChunk);
+    };
     auto meta = std::shared_ptr<CopyTask>(block, block->data());
     meta->ticket = ticket->id_;
     meta->shard_id = b.shard_id;
@@ -580,9 +589,10 @@ std::shared_ptr<CaptureTicket> Engine::capture_impl(std::vector<FileSpec>& files
       t->final_for_segment = k + 1 == b.larges.size();
       dst += b.larges[k].size;
       tasks.push_back(std::move(t));
+      if (tasks.size() == kSubmitChunk) submit();
     }
     tr.mark("reserve+register+tasks");
-    transfers_.submit_copies(ticket->id_, std::move(tasks));
+    submit();
     tr.mark("submit");
     total += b.payload;
   }

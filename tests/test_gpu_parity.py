@@ -81,6 +81,25 @@ def test_files_match_reference_and_oracle(gpu, oracle, cases, fixtures, tmp_path
         shutil.rmtree(root, ignore_errors=True)
 
 
+@pytest.mark.parametrize("variant", ["default", "kernel-only", "copy-engine-only"])
+def test_many_small_leaves_submitted_in_chunks(gpu, oracle, tmp_path, variant):
+    """3000 x 4 KiB leaves, all above the threshold: one file's tasks are
+    submitted in chunks of 1024 while the rest are built (engine.cpp); the
+    file must still equal the oracle's composition and the ticket's device
+    time must span all chunks."""
+    lz = gpu
+    from paper_2406_10707_b200.workloads import sweep_class
+    w = sweep_class(4096, 3000 * 4096)
+    eng, built, t = run_capture(lz, w, 4096, tmp_path / "many", str(tmp_path), **VARIANTS[variant])
+    expect = oracle.compose_files(w, 4096)
+    got = {os.path.relpath(f, tmp_path / "many"): f for f in t.shard_files()}
+    assert set(got) == set(expect)
+    for rel, path in got.items():
+        assert np.array_equal(np.fromfile(path, dtype=np.uint8), expect[rel]), rel
+    assert eng.ticket_device_ms(t) > 0
+    eng.close()
+
+
 def test_c1_golden_digests_and_restore(gpu, oracle, tmp_path):
     lz = gpu
     from paper_2406_10707_b200.workloads import gpt2_small
